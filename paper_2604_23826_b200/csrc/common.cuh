@@ -1,0 +1,90 @@
+// common.cuh — shared device-side definitions of the B200 sufficient-statistics engine.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sstat_b200 {
+
+// Rows per accumulation tile.  A tile is the deterministic unit of work: its
+// partial depends only on the rows of the tile, so results are bit-identical for
+// any grid size, GPU count or staging layout.  4096 rows x 8 warps x 128 k-steps.
+constexpr uint32_t kTileRows = 4096;
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kTileKsteps = kTileRows / 4 / kWarps;  // k-steps per warp per tile
+
+// Number of doubles in one canonical partial: sums[p] then the packed upper triangle.
+__host__ __device__ inline uint64_t partial_len(uint32_t p) { return p + (uint64_t)p * (p + 1) / 2; }
+
+// SymPacked index (linalg.hpp:58-61), j <= k.
+__host__ __device__ inline uint32_t packed_index(uint32_t p, uint32_t j, uint32_t k) {
+    return j * p - j * (j - 1) / 2 + (k - j);
+}
+
+// Everything a tile kernel needs for one launch.  `base` points at the row with
+// absolute index `base_row` (device shard or a staging slot).
+struct TileJob {
+    const double* base;
+    uint64_t base_row;
+    const uint64_t* range_start;   // [n_ranges] absolute first row of each local range
+    const uint64_t* range_count;   // [n_ranges]
+    const uint64_t* tile_prefix;   // [n_ranges + 1] local range r owns tiles [prefix[r], prefix[r+1])
+    const double* shift;           // [n_ranges][p] first row of each range, or nullptr
+    uint32_t n_ranges;
+    uint32_t p;
+    uint64_t tile_begin, tile_end; // tiles of this launch
+    double* tile_partials;         // [n_tiles][partial_len(p)] canonical, shifted space
+};
+
+// Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).
+__device__ __forceinline__ uint32_t range_of_tile(const uint64_t* prefix, uint32_t n_ranges, uint64_t t) {
+    uint32_t lo = 0, hi = n_ranges;  // invariant: prefix[lo] <= t < prefix[hi]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(prefix + mid) <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// FP64 warp MMA D = A(8x4, row) * B(4x8, col) + C on the DMMA tensor pipe.
+// Fragments (PTX ISA, mma.m8n8k4 .f64): lane l, g = l>>2, k = l&3 holds
+//   A[g][k], B[k][g], C[g][2k], C[g][2k+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Streaming 64/128-bit loads: read once, evict first.
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
+
+// Per-rank header in front of the range partials: [0] lowest failing global range
+// (UINT64_MAX = none), [1] first non-finite linear index row*p + col.
+constexpr uint32_t kHdr = 4;
+
+// The ascending range fold of one entry (reference include/sstat/reduce.hpp:142-145 with
+// merge_suffstats, src/suffstats.cpp:86-105): acc starts at +0.0 and adds range 0, 1, ...
+// Range r sits in rank q = owner(r), first(q) = floor(q R / W), at
+//   buf + q*rank_stride + kHdr + (r - first(q))*E + e.
+// Binary32 mode rounds every add through float like merge_suffstats.  Shared by the
+// device fold (K3b) and the host fold used to check the rank layout.
+__host__ __device__ inline double fold_entry(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world,
+                                             uint32_t p, uint32_t precision, uint64_t e) {
+    const uint64_t E = partial_len(p);
+    double acc = 0.0;
+    for (int q = 0; q < world; ++q) {
+        const uint64_t f = (uint64_t)q * n_ranges / world, l = (uint64_t)(q + 1) * n_ranges / world;
+        const double* part = buf + (uint64_t)q * rank_stride + kHdr + e;
+        if (precision == 1) {
+            for (uint64_t r = 0; r < l - f; ++r) acc = (double)((float)acc + (float)part[r * E]);
+        } else {
+            for (uint64_t r = 0; r < l - f; ++r) acc += part[r * E];
+        }
+    }
+    return acc;
+}
+
+}  // namespace sstat_b200

@@ -1,0 +1,989 @@
+// engine.cu — host runtime and C ABI of the B200 sufficient-statistics engine.
+//
+// Replaces the reference's parallel reduction engine for the sufficient-statistics
+// path (reference include/sstat/reduce.hpp:70-146 run_reduction, src/suffstats.cpp:279-288
+// dataset_suffstats):  the std::thread pool pulling ranges becomes HBM-resident (or
+// streamed) row shards accumulated tile by tile by K1/K2, the per-range partial slots
+// become a device buffer of per-range partials (K3a), and the ascending range fold
+// becomes K3b — run after an NCCL all-gather when rows are sharded over GPUs.
+// Results are a fixed function of (data, plan): bit-identical for any GPU count,
+// grid size or staging layout.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/sstat_cuda.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace sstat_b200;
+
+namespace {
+
+constexpr uint64_t kNone = ~0ull;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(n, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(n, 256);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+struct sstat_cuda_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr, stream = nullptr, copy = nullptr;
+    std::mutex mu;
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags;
+    HostBuf h_meta, h_result, h_shift, h_flags;
+    uint32_t n_slots = 4;
+    uint64_t slot_bytes = 256ull << 20;
+    std::vector<DevBuf> slots;
+    std::vector<HostBuf> bounce;
+    std::vector<cudaEvent_t> ev_copied, ev_free;
+    cudaEvent_t ev[6] = {};
+};
+
+namespace {
+
+// ---- error plumbing ----
+struct Fail {
+    int status;
+    std::string msg;
+    uint64_t row = 0, range = 0;
+    uint32_t col = 0;
+};
+
+int report(sstat_cuda_error* err, const Fail& f) {
+    if (err) {
+        err->status = (uint32_t)f.status;
+        err->row = f.row;
+        err->col = f.col;
+        err->range_index = f.range;
+        std::snprintf(err->msg, sizeof err->msg, "%s", f.msg.c_str());
+    }
+    return f.status;
+}
+
+Fail cuda_fail(cudaError_t e, const char* what) {
+    Fail f;
+    f.status = (e == cudaErrorMemoryAllocation) ? SSTAT_ERR_OOM : SSTAT_ERR_CUDA;
+    f.msg = std::string(what) + ": " + cudaGetErrorString(e);
+    return f;
+}
+
+#define CUDA_TRY(expr)                                       \
+    do {                                                     \
+        cudaError_t e_ = (expr);                             \
+        if (e_ != cudaSuccess) throw cuda_fail(e_, #expr);   \
+    } while (0)
+
+// ---- SSTATBIN (reference include/sstat/binfile.hpp:17-29): 64-byte header, payload at 64 ----
+struct BinFile {
+    int fd = -1;
+    uint64_t rows = 0;
+    uint32_t cols = 0;
+    ~BinFile() {
+        if (fd >= 0) ::close(fd);
+    }
+};
+
+uint64_t le64(const unsigned char* b) {
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+    return v;
+}
+uint32_t le32(const unsigned char* b) { return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24); }
+
+// Header and size validation, with the reference's error classes (binfile.cpp:24-47,122-138).
+void open_bin(const char* path, BinFile& f) {
+    Fail io{SSTAT_ERR_IO, ""}, fmt{SSTAT_ERR_FORMAT, ""};
+    struct stat st;
+    if (!path || ::stat(path, &st) != 0) {
+        io.msg = std::string("no such file: ") + (path ? path : "(null)");
+        throw io;
+    }
+    f.fd = ::open(path, O_RDONLY);
+    if (f.fd < 0) {
+        io.msg = std::string("cannot open ") + path;
+        throw io;
+    }
+    unsigned char h[64];
+    if (::pread(f.fd, h, 64, 0) != 64) {
+        fmt.msg = std::string("file too small for header: ") + path;
+        throw fmt;
+    }
+    if (std::memcmp(h, "SSTATBIN", 8) != 0) {
+        fmt.msg = "bad magic: not a binary dataset file";
+        throw fmt;
+    }
+    const uint32_t version = le32(h + 8);
+    if (version != 1) {
+        fmt.msg = "unsupported format version " + std::to_string(version);
+        throw fmt;
+    }
+    f.rows = le64(h + 12);
+    f.cols = le32(h + 20);
+    const uint64_t checksum = le64(h + 24);
+    const uint32_t flags = le32(h + 32);
+    if (flags & ~1u) {
+        fmt.msg = "unknown header flags";
+        throw fmt;
+    }
+    if (!(flags & 1u) && checksum != 0) {
+        fmt.msg = "checksum field set without checksum flag";
+        throw fmt;
+    }
+    for (int i = 36; i < 64; ++i)
+        if (h[i] != 0) {
+            fmt.msg = "reserved header bytes are not zero";
+            throw fmt;
+        }
+    if (f.cols == 0) {
+        fmt.msg = "column count is zero";
+        throw fmt;
+    }
+    const uint64_t expect = 64 + f.rows * (uint64_t)f.cols * 8;
+    if ((uint64_t)st.st_size != expect) {
+        fmt.msg = std::string("file size mismatch in ") + path + ": header implies " + std::to_string(expect) +
+                  " bytes, file has " + std::to_string((uint64_t)st.st_size);
+        throw fmt;
+    }
+}
+
+void read_exact(int fd, void* dst, uint64_t bytes, uint64_t offset) {
+    char* d = static_cast<char*>(dst);
+    while (bytes) {
+        const ssize_t got = ::pread(fd, d, bytes > (1ull << 30) ? (1ull << 30) : bytes, (off_t)offset);
+        if (got <= 0) throw Fail{SSTAT_ERR_FORMAT, "truncated read"};
+        d += got;
+        bytes -= (uint64_t)got;
+        offset += (uint64_t)got;
+    }
+}
+
+// Row source abstraction for host-side staging.
+struct HostRows {
+    const sstat_cuda_source* src;
+    BinFile* file;
+    uint32_t p;
+    bool pinned;
+    const double* host_row(uint64_t row) const {
+        return static_cast<const double*>(src->ptr) + (row - src->first_row) * p;
+    }
+    // copy rows [row, row + n) into dst (pageable ptr / file)
+    void fill(void* dst, uint64_t row, uint64_t n) const {
+        if (file) read_exact(file->fd, dst, n * p * 8, 64 + row * p * 8);
+        else std::memcpy(dst, host_row(row), n * p * 8);
+    }
+};
+
+void ensure_slots(sstat_cuda_ctx* c, bool need_bounce) {
+    if (c->slots.size() != c->n_slots) {
+        for (auto& s : c->slots) s.release();
+        for (auto& b : c->bounce) b.release();
+        for (auto e : c->ev_copied) cudaEventDestroy(e);
+        for (auto e : c->ev_free) cudaEventDestroy(e);
+        c->slots.assign(c->n_slots, DevBuf{});
+        c->bounce.assign(c->n_slots, HostBuf{});
+        c->ev_copied.assign(c->n_slots, nullptr);
+        c->ev_free.assign(c->n_slots, nullptr);
+        for (uint32_t i = 0; i < c->n_slots; ++i) {
+            CUDA_TRY(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
+        }
+    }
+    for (uint32_t i = 0; i < c->n_slots; ++i) {
+        CUDA_TRY(c->slots[i].reserve(c->slot_bytes));
+        if (need_bounce) CUDA_TRY(c->bounce[i].reserve(c->slot_bytes));
+    }
+}
+
+enum class Mode { Dataset, Chunk, Partials };
+
+struct Plan {
+    Mode mode = Mode::Dataset;
+    uint64_t want_r0 = 0, want_r1 = 0;  // Mode::Partials: ranges to accumulate
+    double* partials_host = nullptr;    // Mode::Partials: [(want_r1 - want_r0) * E]
+    uint32_t p, precision, flags;
+    uint64_t R, r0, r1, L, lmax, E, n_tiles, total, span_begin, span_end;
+    const uint64_t* starts;
+    const uint64_t* counts;
+    std::vector<uint64_t> tile_row, tile_rows;  // host view of local tiles (streaming)
+};
+
+uint64_t tiles_of(uint64_t count) { return (count + kTileRows - 1) / kTileRows; }
+
+struct Outcome {
+    uint64_t bad_lin = kNone;  // lowest first-non-finite linear index over all ranks
+};
+
+// Streams the rows of tiles [t0, t1) (or whole ranges for refexact) through the staging ring.
+// `launch(base, base_row, first_tile, last_tile)` enqueues the kernel for one chunk.
+template <class Launch>
+void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint64_t>& unit_row,
+                   const std::vector<uint64_t>& unit_rows, Launch&& launch, sstat_cuda_timings* tm) {
+    const uint64_t row_bytes = (uint64_t)hr.p * 8;
+    const uint64_t n_units = unit_row.size();
+    uint64_t u = 0, chunk = 0;
+    while (u < n_units) {
+        // maximal run of row-contiguous units fitting one slot
+        uint64_t v = u, bytes = 0;
+        while (v < n_units) {
+            const uint64_t b = unit_rows[v] * row_bytes;
+            if (v > u && (bytes + b > c->slot_bytes || unit_row[v] != unit_row[v - 1] + unit_rows[v - 1])) break;
+            if (b > c->slot_bytes) throw Fail{SSTAT_ERR_UNSUPPORTED, "staging slot smaller than one work unit"};
+            bytes += b;
+            ++v;
+        }
+        const uint32_t slot = (uint32_t)(chunk % c->n_slots);
+        const uint64_t row0 = unit_row[u], nrows = bytes / row_bytes;
+        CUDA_TRY(cudaStreamWaitEvent(c->copy, c->ev_free[slot], 0));
+        const void* host_src;
+        if (hr.pinned) {
+            host_src = hr.host_row(row0);
+        } else {
+            // the bounce buffer of this slot is reused: its previous copy must be done
+            if (chunk >= c->n_slots) CUDA_TRY(cudaEventSynchronize(c->ev_copied[slot]));
+            hr.fill(c->bounce[slot].p, row0, nrows);
+            host_src = c->bounce[slot].p;
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->slots[slot].p, host_src, bytes, cudaMemcpyHostToDevice, c->copy));
+        CUDA_TRY(cudaEventRecord(c->ev_copied[slot], c->copy));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_copied[slot], 0));
+        launch(static_cast<const double*>(c->slots[slot].p), row0, u, v);
+        CUDA_TRY(cudaEventRecord(c->ev_free[slot], c->stream));
+        if (tm) {
+            tm->h2d_bytes += bytes;
+            tm->kernel_launches += 1;
+        }
+        u = v;
+        ++chunk;
+    }
+}
+
+void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile& file) {
+    const bool single_chunk = P.mode != Mode::Dataset;
+    Fail inv{SSTAT_ERR_INVALID, ""};
+    if (P.p == 0) {
+        inv.msg = "schema: column count must be >= 1";
+        throw inv;
+    }
+    if (P.precision > 1) {
+        inv.msg = "unknown precision mode";
+        throw inv;
+    }
+    if (P.R > 0 && (!P.starts || !P.counts)) {
+        inv.msg = "null range arrays";
+        throw inv;
+    }
+    P.total = 0;
+    for (uint64_t i = 0; i < P.R; ++i) {
+        if (i > 0 && P.starts[i] < P.starts[i - 1] + P.counts[i - 1]) {
+            inv.msg = "partition ranges must be ascending and disjoint";
+            throw inv;
+        }
+        P.total += P.counts[i];
+    }
+    const int world = single_chunk ? 1 : c->world;
+    if (src->kind == SSTAT_SRC_FILE) {
+        open_bin(src->path, file);
+        if (file.rows != P.total) {
+            inv.msg = "run_reduction: partition covers " + std::to_string(P.total) + " rows but dataset has " +
+                      std::to_string(file.rows);
+            throw inv;
+        }
+        if (file.cols != P.p) {
+            Fail f{SSTAT_ERR_SCHEMA, "range 0 failed: chunk has " + std::to_string(file.cols) + " columns, schema has " +
+                                         std::to_string(P.p)};
+            f.range = 0;
+            throw f;
+        }
+    } else if (src->kind == SSTAT_SRC_DEVICE || src->kind == SSTAT_SRC_HOST) {
+        if (!src->ptr && P.total > 0) {
+            inv.msg = "null row pointer";
+            throw inv;
+        }
+        if (world == 1 && P.mode == Mode::Dataset) {
+            const uint64_t ds = src->first_row + src->n_rows;
+            if (src->first_row != 0 || ds != P.total) {
+                inv.msg = "run_reduction: partition covers " + std::to_string(P.total) + " rows but dataset has " +
+                          std::to_string(src->n_rows) + " rows";
+                throw inv;
+            }
+        }
+    } else {
+        inv.msg = "unknown source kind";
+        throw inv;
+    }
+    uint64_t ds_rows = kNone;  // dataset rows when known to this rank
+    if (src->kind == SSTAT_SRC_FILE) ds_rows = file.rows;
+    else if (world == 1 && P.mode == Mode::Dataset) ds_rows = src->first_row + src->n_rows;
+    if (P.R > 0 && ds_rows != kNone && P.starts[P.R - 1] + P.counts[P.R - 1] > ds_rows) {
+        inv.msg = "partition exceeds the dataset";
+        throw inv;
+    }
+    P.r0 = (uint64_t)c->rank * P.R / world;
+    P.r1 = (uint64_t)(c->rank + 1) * P.R / world;
+    if (world == 1) {
+        P.r0 = 0;
+        P.r1 = P.R;
+    }
+    if (P.mode == Mode::Partials) {
+        if (P.want_r0 > P.want_r1 || P.want_r1 > P.R) {
+            inv.msg = "range window out of bounds";
+            throw inv;
+        }
+        P.r0 = P.want_r0;
+        P.r1 = P.want_r1;
+    }
+    P.L = P.r1 - P.r0;
+    P.lmax = (P.R + world - 1) / world;
+    P.E = partial_len(P.p);
+    P.span_begin = P.L ? P.starts[P.r0] : 0;
+    P.span_end = P.L ? P.starts[P.r1 - 1] + P.counts[P.r1 - 1] : 0;
+    if (src->kind != SSTAT_SRC_FILE && P.L > 0 &&
+        (P.span_begin < src->first_row || P.span_end > src->first_row + src->n_rows)) {
+        inv.msg = "source rows [" + std::to_string(src->first_row) + ", " + std::to_string(src->first_row + src->n_rows) +
+                  ") do not cover this rank's ranges [" + std::to_string(P.span_begin) + ", " +
+                  std::to_string(P.span_end) + ")";
+        throw inv;
+    }
+    if (P.L > 65535 && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1)) {
+        inv.msg = "reference-order mode supports at most 65535 ranges per device";
+        throw inv;
+    }
+}
+
+// The engine proper.  Returns the all-rank outcome; throws Fail.
+void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
+         sstat_cuda_timings* tm) {
+    BinFile file;
+    check_plan(c, src, P, file);
+    const int world = P.mode == Mode::Dataset ? c->world : 1;
+    const bool refexact = (P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1;
+    const bool shift = !(P.flags & SSTAT_FLAG_NO_SHIFT) && !refexact;
+    const uint32_t p = P.p;
+    const uint64_t E = P.E, L = P.L;
+    cudaStream_t s = c->stream;
+
+    // ---- local plan → device ----
+    CUDA_TRY(c->h_meta.reserve((3 * L + 1) * 8));
+    uint64_t* hm = c->h_meta.as<uint64_t>();
+    uint64_t nt = 0;
+    for (uint64_t i = 0; i < L; ++i) {
+        hm[i] = P.starts[P.r0 + i];
+        hm[L + i] = P.counts[P.r0 + i];
+        hm[2 * L + i] = nt;
+        nt += tiles_of(P.counts[P.r0 + i]);
+    }
+    hm[3 * L] = nt;
+    P.n_tiles = nt;
+    CUDA_TRY(c->d_meta.reserve((3 * L + 1) * 8));
+    uint64_t* d_starts = c->d_meta.as<uint64_t>();
+    uint64_t* d_counts = d_starts + L;
+    uint64_t* d_prefix = d_starts + 2 * L;
+    CUDA_TRY(cudaMemcpyAsync(d_starts, hm, (3 * L + 1) * 8, cudaMemcpyHostToDevice, s));
+
+    const uint64_t rank_stride = kHdr + P.lmax * E;
+    CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
+    CUDA_TRY(c->d_flags.reserve(std::max<uint64_t>(L, 1) * 4));
+    CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, kHdr * 8, s));
+    CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
+    double* rank_buf = c->d_rank.as<double>();
+    uint32_t* d_flags = c->d_flags.as<uint32_t>();
+    if (!refexact) {
+        CUDA_TRY(c->d_tiles.reserve(std::max<uint64_t>(nt, 1) * E * 8));
+        if (shift) CUDA_TRY(c->d_shift.reserve(std::max<uint64_t>(L, 1) * p * 8));
+    }
+    const double* d_shift = shift ? c->d_shift.as<double>() : nullptr;
+    const bool wide = p > 64;
+
+    auto tile_job = [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
+        TileJob j;
+        j.base = base;
+        j.base_row = base_row;
+        j.range_start = d_starts;
+        j.range_count = d_counts;
+        j.tile_prefix = d_prefix;
+        j.shift = d_shift;
+        j.n_ranges = (uint32_t)L;
+        j.p = p;
+        j.tile_begin = t0;
+        j.tile_end = t1;
+        j.tile_partials = c->d_tiles.as<double>();
+        CUDA_TRY(wide ? launch_widep(j, c->sms, s) : launch_smallp(j, c->sms, s));
+    };
+
+    CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    if (tm) tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
+    if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
+        const double* base = static_cast<const double*>(src->ptr);
+        const uint64_t base_row = src->first_row;
+        if (refexact) {
+            CUDA_TRY(launch_refexact(base, base_row, d_starts, d_counts, (uint32_t)L, p, P.precision, P.r0, rank_buf,
+                                     rank_buf + kHdr, d_flags, s));
+            CUDA_TRY(cudaEventRecord(c->ev[1], s));
+            if (tm) tm->kernel_launches += 1;
+        } else {
+            if (shift) CUDA_TRY(launch_gather_shift(base, base_row, d_starts, d_counts, (uint32_t)L, p, c->d_shift.as<double>(), s));
+            CUDA_TRY(cudaEventRecord(c->ev[0], s));  // kernel_seconds brackets K1/K2 alone
+            if (nt > 0) tile_job(base, base_row, 0, nt);
+            CUDA_TRY(cudaEventRecord(c->ev[1], s));
+            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, (uint32_t)L, p, P.r0,
+                                       rank_buf, d_flags, s));
+            if (tm) tm->kernel_launches += 2 + (shift ? 1 : 0);
+        }
+        CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_counts, (uint32_t)L, p, d_flags, rank_buf,
+                                       c->sms * 2, s));
+        CUDA_TRY(cudaEventRecord(c->ev[2], s));
+        if (tm) tm->kernel_launches += 1;
+    } else if (L > 0) {
+        // ---- host / file source: pinned staging ring, copy stream || compute stream ----
+        cudaPointerAttributes attr{};
+        bool pinned = false;
+        if (src->kind == SSTAT_SRC_HOST) {
+            if (cudaPointerGetAttributes(&attr, src->ptr) == cudaSuccess)
+                pinned = attr.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+        }
+        HostRows hr{src, src->kind == SSTAT_SRC_FILE ? &file : nullptr, p, pinned};
+        ensure_slots(c, !pinned);
+        if (shift) {
+            CUDA_TRY(c->h_shift.reserve(L * p * 8));
+            double* hs = c->h_shift.as<double>();
+            for (uint64_t i = 0; i < L; ++i) {
+                if (P.counts[P.r0 + i] == 0) std::fill(hs + i * p, hs + (i + 1) * p, 0.0);
+                else if (file.fd >= 0) hr.fill(hs + i * p, P.starts[P.r0 + i], 1);
+                else std::memcpy(hs + i * p, hr.host_row(P.starts[P.r0 + i]), p * 8);
+            }
+            CUDA_TRY(cudaMemcpyAsync(c->d_shift.p, hs, L * p * 8, cudaMemcpyHostToDevice, s));
+        }
+        CUDA_TRY(cudaEventRecord(c->ev[0], s));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy, c->ev[0], 0));
+        if (refexact) {
+            // units = whole ranges; each chunk launches the sequential chains of its ranges
+            std::vector<uint64_t> urow(L), urows(L);
+            for (uint64_t i = 0; i < L; ++i) {
+                urow[i] = P.starts[P.r0 + i];
+                urows[i] = P.counts[P.r0 + i];
+            }
+            stream_chunks(c, hr, urow, urows,
+                          [&](const double* base, uint64_t base_row, uint64_t u0, uint64_t u1) {
+                              // ranges [u0, u1) of this chunk → partial slots u0 .. u1-1
+                              CUDA_TRY(launch_refexact(base, base_row, d_starts + u0, d_counts + u0, (uint32_t)(u1 - u0),
+                                                       p, P.precision, P.r0 + u0, rank_buf, rank_buf + kHdr + u0 * E,
+                                                       d_flags + u0, s));
+                          },
+                          tm);
+            CUDA_TRY(cudaEventRecord(c->ev[1], s));
+        } else {
+            std::vector<uint64_t> trow(nt), trows(nt);
+            for (uint64_t i = 0, t = 0; i < L; ++i) {
+                const uint64_t rs = P.starts[P.r0 + i], rc = P.counts[P.r0 + i];
+                for (uint64_t q = 0; q < tiles_of(rc); ++q, ++t) {
+                    trow[t] = rs + q * kTileRows;
+                    trows[t] = std::min<uint64_t>(kTileRows, rs + rc - trow[t]);
+                }
+            }
+            stream_chunks(c, hr, trow, trows,
+                          [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
+                              tile_job(base, base_row, t0, t1);
+                          },
+                          tm);
+            CUDA_TRY(cudaEventRecord(c->ev[1], s));
+            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, (uint32_t)L, p, P.r0,
+                                       rank_buf, d_flags, s));
+        }
+        // Non-finite localisation: re-stream only the flagged ranges (error path).
+        CUDA_TRY(c->h_flags.reserve(L * 4));
+        CUDA_TRY(cudaMemcpyAsync(c->h_flags.p, d_flags, L * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const uint32_t* hf = c->h_flags.as<uint32_t>();
+        bool any = false;
+        for (uint64_t i = 0; i < L; ++i) any |= hf[i] != 0;
+        if (any) {
+            // header[0] flags the rank for the scan kernel
+            uint64_t lowest = kNone;
+            for (uint64_t i = 0; i < L && lowest == kNone; ++i)
+                if (hf[i]) lowest = P.r0 + i;
+            CUDA_TRY(cudaMemcpyAsync(rank_buf, &lowest, 8, cudaMemcpyHostToDevice, s));
+            for (uint64_t i = 0; i < L; ++i) {
+                if (!hf[i]) continue;
+                std::vector<uint64_t> urow{P.starts[P.r0 + i]}, urows{P.counts[P.r0 + i]};
+                // split the range into slot-sized pieces of whole rows
+                std::vector<uint64_t> prow, prows;
+                const uint64_t per = std::max<uint64_t>(1, c->slot_bytes / (p * 8));
+                for (uint64_t r = 0; r < urows[0]; r += per) {
+                    prow.push_back(urow[0] + r);
+                    prows.push_back(std::min(per, urows[0] - r));
+                }
+                uint32_t one = 1;
+                CUDA_TRY(cudaMemcpyAsync(d_flags, &one, 4, cudaMemcpyHostToDevice, s));
+                stream_chunks(c, hr, prow, prows,
+                              [&](const double* base, uint64_t base_row, uint64_t u0, uint64_t u1) {
+                                  // scan rows [prow[u0], prow[u1-1]+prows[u1-1]) as a one-range job
+                                  uint64_t hmeta[2] = {prow[u0], 0};
+                                  for (uint64_t k = u0; k < u1; ++k) hmeta[1] += prows[k];
+                                  CUDA_TRY(cudaMemcpyAsync(d_starts, hmeta, 16, cudaMemcpyHostToDevice, s));
+                                  CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_starts + 1, 1, p, d_flags,
+                                                                 rank_buf, c->sms * 2, s));
+                                  CUDA_TRY(cudaStreamSynchronize(s));
+                              },
+                              nullptr);
+            }
+        }
+        CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    } else {
+        CUDA_TRY(cudaEventRecord(c->ev[1], s));
+        CUDA_TRY(cudaEventRecord(c->ev[2], s));
+    }
+
+    if (P.mode == Mode::Partials) {
+        CUDA_TRY(c->h_result.reserve((L * E + kHdr) * 8));
+        double* hres = c->h_result.as<double>();
+        CUDA_TRY(cudaMemcpyAsync(hres, rank_buf, (kHdr + L * E) * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        std::memcpy(&out.bad_lin, hres + 1, 8);
+        if (L) std::memcpy(P.partials_host, hres + kHdr, L * E * 8);
+        return;
+    }
+
+    // ---- exchange (rank-ordered all-gather of per-range partials) ----
+    const double* fold_buf = rank_buf;
+    if (world > 1) {
+        CUDA_TRY(c->d_gather.reserve(rank_stride * world * 8));
+        ncclResult_t r = ncclAllGather(rank_buf, c->d_gather.p, rank_stride, ncclDouble, c->comm, s);
+        if (r != ncclSuccess) throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r)};
+        fold_buf = c->d_gather.as<double>();
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[3], s));
+    CUDA_TRY(c->d_result.reserve(E * 8));
+    CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, c->d_result.as<double>(), s));
+    CUDA_TRY(cudaEventRecord(c->ev[4], s));
+    if (tm) tm->kernel_launches += 1;
+    CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
+    double* hres = c->h_result.as<double>();
+    CUDA_TRY(cudaMemcpyAsync(hres, c->d_result.p, E * 8, cudaMemcpyDeviceToHost, s));
+    for (int q = 0; q < world; ++q)
+        CUDA_TRY(cudaMemcpyAsync(hres + E + q * kHdr, fold_buf + q * rank_stride, kHdr * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaGetLastError());
+    for (int q = 0; q < world; ++q) {
+        uint64_t lin;
+        std::memcpy(&lin, hres + E + q * kHdr + 1, 8);
+        out.bad_lin = std::min(out.bad_lin, lin);
+    }
+    std::memcpy(result_host, hres, E * 8);
+    if (tm) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+        tm->kernel_seconds += ms * 1e-3;
+        cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+        tm->fold_seconds += ms * 1e-3;
+        cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
+        tm->fold_seconds += ms * 1e-3;
+        cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+        tm->exchange_seconds += ms * 1e-3;
+        tm->n_local_ranges = (uint32_t)L;
+    }
+}
+
+uint64_t range_of_row(const Plan& P, uint64_t row) {
+    uint64_t lo = 0, hi = P.R;  // last range with start <= row
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (P.starts[mid] <= row) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+struct Guard {
+    sstat_cuda_ctx* c;
+    std::lock_guard<std::mutex> lk;
+    explicit Guard(sstat_cuda_ctx* ctx) : c(ctx), lk(ctx->mu) { cudaSetDevice(ctx->device); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int sstat_cuda_abi_version(void) { return SSTAT_CUDA_ABI_VERSION; }
+
+const char* sstat_status_string(int status) {
+    switch (status) {
+        case SSTAT_OK: return "ok";
+        case SSTAT_ERR_NONFINITE: return "non-finite value";
+        case SSTAT_ERR_SCHEMA: return "schema mismatch";
+        case SSTAT_ERR_INVALID: return "invalid argument";
+        case SSTAT_ERR_CUDA: return "CUDA error";
+        case SSTAT_ERR_NCCL: return "NCCL error";
+        case SSTAT_ERR_OOM: return "out of device memory";
+        case SSTAT_ERR_UNSUPPORTED: return "unsupported";
+        case SSTAT_ERR_IO: return "I/O error";
+        case SSTAT_ERR_FORMAT: return "format error";
+        default: return "unknown status";
+    }
+}
+
+int sstat_cuda_init(sstat_cuda_ctx** out, int device) {
+    if (!out) return SSTAT_ERR_INVALID;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return SSTAT_ERR_CUDA;
+    }
+    if (device < 0) cudaGetDevice(&device);
+    if (device >= n) return SSTAT_ERR_INVALID;
+    auto* c = new sstat_cuda_ctx;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return SSTAT_ERR_CUDA;
+    }
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return SSTAT_ERR_CUDA;
+    }
+    c->stream = c->own;
+    for (auto& e : c->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            delete c;
+            return SSTAT_ERR_CUDA;
+        }
+    *out = c;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_destroy(sstat_cuda_ctx* c) {
+    if (!c) return SSTAT_OK;
+    {
+        Guard g(c);
+        cudaStreamSynchronize(c->stream);
+        cudaStreamSynchronize(c->copy);
+        if (c->comm) ncclCommDestroy(c->comm);
+        for (DevBuf* b : {&c->d_meta, &c->d_tiles, &c->d_rank, &c->d_gather, &c->d_shift, &c->d_result, &c->d_flags})
+            b->release();
+        for (HostBuf* b : {&c->h_meta, &c->h_result, &c->h_shift, &c->h_flags}) b->release();
+        for (auto& s : c->slots) s.release();
+        for (auto& b : c->bounce) b.release();
+        for (auto e : c->ev_copied) cudaEventDestroy(e);
+        for (auto e : c->ev_free) cudaEventDestroy(e);
+        for (auto e : c->ev) cudaEventDestroy(e);
+        cudaStreamDestroy(c->own);
+        cudaStreamDestroy(c->copy);
+    }
+    delete c;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_set_stream(sstat_cuda_ctx* c, void* stream) {
+    if (!c) return SSTAT_ERR_INVALID;
+    Guard g(c);
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_set_staging(sstat_cuda_ctx* c, uint32_t slots, uint64_t slot_bytes) {
+    if (!c || slots < 2 || slot_bytes < (1u << 20)) return SSTAT_ERR_INVALID;
+    Guard g(c);
+    cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->copy);
+    for (auto& s : c->slots) s.release();
+    for (auto& b : c->bounce) b.release();
+    for (auto e : c->ev_copied) cudaEventDestroy(e);
+    for (auto e : c->ev_free) cudaEventDestroy(e);
+    c->slots.clear();
+    c->bounce.clear();
+    c->ev_copied.clear();
+    c->ev_free.clear();
+    c->n_slots = slots;
+    c->slot_bytes = slot_bytes & ~(uint64_t)127;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_nccl_unique_id(void* id_out, size_t id_bytes) {
+    if (!id_out || id_bytes < sizeof(ncclUniqueId)) return SSTAT_ERR_INVALID;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return SSTAT_ERR_NCCL;
+    std::memcpy(id_out, &id, sizeof id);
+    return SSTAT_OK;
+}
+
+int sstat_cuda_comm_init(sstat_cuda_ctx* c, int rank, int world, const void* id, size_t id_bytes) {
+    if (!c || world < 1 || rank < 0 || rank >= world) return SSTAT_ERR_INVALID;
+    Guard g(c);
+    if (c->comm) {
+        ncclCommDestroy(c->comm);
+        c->comm = nullptr;
+    }
+    c->rank = rank;
+    c->world = world;
+    if (world == 1 && !id) return SSTAT_OK;
+    if (!id || id_bytes < sizeof(ncclUniqueId)) return SSTAT_ERR_INVALID;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    if (ncclCommInitRank(&c->comm, world, uid, rank) != ncclSuccess) {
+        c->comm = nullptr;
+        c->rank = 0;
+        c->world = 1;
+        return SSTAT_ERR_NCCL;
+    }
+    return SSTAT_OK;
+}
+
+int sstat_shard_ranges(uint64_t n_ranges, int rank, int world, uint64_t* first, uint64_t* last) {
+    if (world < 1 || rank < 0 || rank >= world || !first || !last) return SSTAT_ERR_INVALID;
+    *first = (uint64_t)rank * n_ranges / world;
+    *last = (uint64_t)(rank + 1) * n_ranges / world;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_dataset(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t p, const uint64_t* range_start,
+                       const uint64_t* range_count, uint64_t n_ranges, uint32_t precision, uint32_t flags,
+                       uint64_t* n_out, double* sums_out, double* cross_out, sstat_cuda_timings* tm,
+                       sstat_cuda_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!c || !src || !n_out || !sums_out || !cross_out)
+        return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
+    const double t0 = now_s();
+    if (tm) std::memset(tm, 0, sizeof *tm);
+    try {
+        Guard g(c);
+        if (c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
+        Plan P{};
+        P.p = p;
+        P.precision = precision;
+        P.flags = flags;
+        P.R = n_ranges;
+        P.starts = range_start;
+        P.counts = range_count;
+        std::vector<double> result(partial_len(p ? p : 1));
+        Outcome o;
+        run(c, src, P, result.data(), o, tm);
+        if (o.bad_lin != kNone) {
+            Fail f{SSTAT_ERR_NONFINITE, ""};
+            f.row = o.bad_lin / p;
+            f.col = (uint32_t)(o.bad_lin % p);
+            f.range = range_of_row(P, f.row);
+            f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
+                    ", column " + std::to_string(f.col);
+            throw f;
+        }
+        *n_out = P.total;
+        std::memcpy(sums_out, result.data(), p * 8);
+        std::memcpy(cross_out, result.data() + p, (partial_len(p) - p) * 8);
+        if (tm) tm->total_seconds = now_s() - t0;
+        return SSTAT_OK;
+    } catch (const Fail& f) {
+        cudaGetLastError();
+        return report(err, f);
+    } catch (const std::exception& e) {
+        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
+    }
+}
+
+int sstat_cuda_accumulate(sstat_cuda_ctx* c, const double* rows, uint64_t n_rows, uint32_t p, uint64_t start_row,
+                          uint32_t precision, uint32_t flags, uint64_t* n_out, double* sums_out, double* cross_out,
+                          sstat_cuda_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!c || !n_out || !sums_out || !cross_out) return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
+    if (p == 0) return report(err, Fail{SSTAT_ERR_INVALID, "schema: column count must be >= 1"});
+    if (precision > 1) return report(err, Fail{SSTAT_ERR_INVALID, "unknown precision mode"});
+    try {
+        Guard g(c);
+        const uint64_t E = partial_len(p);
+        if (n_rows == 0) {
+            *n_out = 0;
+            std::memset(sums_out, 0, p * 8);
+            std::memset(cross_out, 0, (E - p) * 8);
+            return SSTAT_OK;
+        }
+        if (!rows) throw Fail{SSTAT_ERR_INVALID, "null row pointer"};
+        cudaPointerAttributes attr{};
+        sstat_cuda_source src{};
+        src.kind = SSTAT_SRC_HOST;
+        if (cudaPointerGetAttributes(&attr, rows) == cudaSuccess &&
+            (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged))
+            src.kind = SSTAT_SRC_DEVICE;
+        cudaGetLastError();
+        src.ptr = rows;
+        src.first_row = start_row;
+        src.n_rows = n_rows;
+        uint64_t rs = start_row, rc = n_rows;
+        Plan P{};
+        P.mode = Mode::Chunk;
+        P.p = p;
+        P.precision = precision;
+        P.flags = flags;
+        P.R = 1;
+        P.starts = &rs;
+        P.counts = &rc;
+        std::vector<double> result(E);
+        Outcome o;
+        run(c, &src, P, result.data(), o, nullptr);
+        if (o.bad_lin != kNone) {
+            Fail f{SSTAT_ERR_NONFINITE, ""};
+            f.row = o.bad_lin / p;
+            f.col = (uint32_t)(o.bad_lin % p);
+            f.range = 0;
+            f.msg = "non-finite value at row " + std::to_string(f.row) + ", column " + std::to_string(f.col);
+            throw f;
+        }
+        *n_out = n_rows;
+        std::memcpy(sums_out, result.data(), p * 8);
+        std::memcpy(cross_out, result.data() + p, (E - p) * 8);
+        return SSTAT_OK;
+    } catch (const Fail& f) {
+        cudaGetLastError();
+        return report(err, f);
+    } catch (const std::exception& e) {
+        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
+    }
+}
+
+int sstat_cuda_range_partials(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t p,
+                              const uint64_t* range_start, const uint64_t* range_count, uint64_t n_ranges,
+                              uint64_t first_range, uint64_t last_range, uint32_t precision, uint32_t flags,
+                              double* partials_out, sstat_cuda_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!c || !src || (!partials_out && last_range > first_range))
+        return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
+    try {
+        Guard g(c);
+        Plan P{};
+        P.mode = Mode::Partials;
+        P.want_r0 = first_range;
+        P.want_r1 = last_range;
+        P.partials_host = partials_out;
+        P.p = p;
+        P.precision = precision;
+        P.flags = flags;
+        P.R = n_ranges;
+        P.starts = range_start;
+        P.counts = range_count;
+        Outcome o;
+        run(c, src, P, nullptr, o, nullptr);
+        if (o.bad_lin != kNone) {
+            Fail f{SSTAT_ERR_NONFINITE, ""};
+            f.row = o.bad_lin / p;
+            f.col = (uint32_t)(o.bad_lin % p);
+            f.range = range_of_row(P, f.row);
+            f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
+                    ", column " + std::to_string(f.col);
+            throw f;
+        }
+        return SSTAT_OK;
+    } catch (const Fail& f) {
+        cudaGetLastError();
+        return report(err, f);
+    } catch (const std::exception& e) {
+        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
+    }
+}
+
+int sstat_fold_ranges_host(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
+                           uint32_t precision, double* out) {
+    if (!buf || !out || world < 1 || p == 0 || precision > 1) return SSTAT_ERR_INVALID;
+    const uint64_t E = partial_len(p);
+    for (uint64_t e = 0; e < E; ++e) out[e] = fold_entry(buf, rank_stride, n_ranges, world, p, precision, e);
+    return SSTAT_OK;
+}
+
+uint64_t sstat_plan_partitions(uint64_t n_rows, uint64_t chunk_rows, uint64_t* starts, uint64_t* counts) {
+    if (chunk_rows == 0 || n_rows == 0) return 0;
+    const uint64_t R = (n_rows + chunk_rows - 1) / chunk_rows;
+    if (starts && counts)
+        for (uint64_t i = 0; i < R; ++i) {
+            starts[i] = i * chunk_rows;
+            counts[i] = std::min(chunk_rows, n_rows - starts[i]);
+        }
+    return R;
+}
+
+int sstat_merge(uint32_t p, uint32_t precision, uint64_t* n_a, double* sums_a, double* cross_a, uint64_t n_b,
+                const double* sums_b, const double* cross_b) {
+    if (!n_a || !sums_a || !cross_a || !sums_b || !cross_b || p == 0 || precision > 1) return SSTAT_ERR_INVALID;
+    const uint64_t np = (uint64_t)p * (p + 1) / 2;
+    *n_a += n_b;
+    if (precision == 1) {
+        for (uint32_t j = 0; j < p; ++j) sums_a[j] = (double)((float)sums_a[j] + (float)sums_b[j]);
+        for (uint64_t i = 0; i < np; ++i) cross_a[i] = (double)((float)cross_a[i] + (float)cross_b[i]);
+    } else {
+        for (uint32_t j = 0; j < p; ++j) sums_a[j] += sums_b[j];
+        for (uint64_t i = 0; i < np; ++i) cross_a[i] += cross_b[i];
+    }
+    return SSTAT_OK;
+}
+
+int sstat_cuda_generate(sstat_cuda_ctx* c, double* dst, uint32_t kind, uint64_t seed, double mu, uint32_t n_int,
+                        uint64_t first_row, uint64_t n_rows, uint32_t p) {
+    if (!c || (!dst && n_rows) || p == 0 || kind > 2) return SSTAT_ERR_INVALID;
+    Guard g(c);
+    cudaError_t e = launch_generate(dst, kind, seed, mu, n_int, first_row, n_rows, p, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    return e == cudaSuccess ? SSTAT_OK : SSTAT_ERR_CUDA;
+}
+
+}  // extern "C"

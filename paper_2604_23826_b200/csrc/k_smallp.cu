@@ -1,0 +1,218 @@
+// k_smallp.cu — K1: streaming sufficient statistics for p <= 64 on the FP64 DMMA pipe.
+//
+// Replaces accumulate_into<double> (reference src/suffstats.cpp:50-70) for one
+// accumulation tile of kTileRows rows.  Each warp walks k-steps of 4 rows.  Lane
+// l = 4g + k loads the values of row k at the NB columns col(J, g), J < NB, straight
+// from HBM with coalesced streaming loads (a warp load covers 4 whole rows), subtracts
+// the range shift c, and feeds the same register as the A fragment (A[g][k]) of
+// column block J and the B fragment (B[k][g]) of column block K of
+//     mma.sync.m8n8k4.f64:  C_JK[m][n] += sum_k X[k][col(J,m)] * X[k][col(K,n)].
+// The NB(NB+1)/2 upper blocks C_JK (J <= K) cover every column pair exactly once (the
+// diagonal blocks twice, symmetrically), so no value is loaded twice and no shared
+// memory is touched in the main loop.  Column sums accumulate with DADD on the same
+// registers.  The epilogue reduces the 8 warps through shared memory in fixed order
+// and writes the tile partial in canonical (sums, SymPacked) order.
+//
+// Column permutation col(J, g):  VEC (p == 8*NB, NB even): g*NB + J  — each lane reads
+// NB contiguous doubles with 128-bit loads;  otherwise J*8 + g — 8 lanes read 8
+// consecutive doubles of a row per instruction (64-byte segments).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sstat_b200 {
+namespace {
+
+template <int NB, bool VEC>
+struct SmallP {
+    static constexpr int NBLK = NB * (NB + 1) / 2;
+    static constexpr int U = NB <= 2 ? (VEC || NB == 1 ? 16 : 8) : (NB <= 4 ? 8 : 4);  // k-steps in flight per warp
+    static constexpr int FRAG = NBLK * 64 + NB * 8;                // per-warp epilogue values
+    __device__ __forceinline__ static int col(int J, int g) { return VEC ? g * NB + J : J * 8 + g; }
+};
+
+template <int NB, bool VEC>
+__device__ __forceinline__ void load_row(const double* __restrict__ rowp, int g, uint32_t p, double (&x)[NB]) {
+    using C = SmallP<NB, VEC>;
+    if constexpr (VEC) {
+        const double* q = rowp + g * NB;
+#pragma unroll
+        for (int i = 0; i < NB / 2; ++i) {
+            const double2 v = ld_stream2(q + 2 * i);
+            x[2 * i] = v.x;
+            x[2 * i + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int J = 0; J < NB; ++J) {
+            const int c = C::col(J, g);
+            x[J] = (c < (int)p) ? ld_stream(rowp + c) : 0.0;
+        }
+    }
+}
+
+template <int NB>
+__device__ __forceinline__ void step(const double (&x)[NB], const double (&c)[NB], double (&acc)[NB * (NB + 1) / 2][2],
+                                     double (&s)[NB]) {
+    double d[NB];
+#pragma unroll
+    for (int J = 0; J < NB; ++J) {
+        d[J] = x[J] - c[J];
+        s[J] += d[J];
+    }
+    int b = 0;
+#pragma unroll
+    for (int J = 0; J < NB; ++J)
+#pragma unroll
+        for (int K = J; K < NB; ++K, ++b) dmma_8x8x4(acc[b][0], acc[b][1], d[J], d[K]);
+}
+
+// Canonical destination of epilogue value e, or -1 when it is padding or the lower
+// mirror of a diagonal block.
+template <int NB, bool VEC>
+__device__ int canonical_slot(int e, uint32_t p) {
+    using C = SmallP<NB, VEC>;
+    if (e < C::NBLK * 64) {
+        int b = e >> 6;
+        const int l = (e & 63) >> 1, m = l >> 2, n = 2 * (l & 3) + (e & 1);
+        int J = 0;
+        while (b >= NB - J) {
+            b -= NB - J;
+            ++J;
+        }
+        const int K = J + b;
+        const int a = C::col(J, m), bb = C::col(K, n);
+        if (a >= (int)p || bb >= (int)p) return -1;
+        if (J == K && a > bb) return -1;
+        const int j = a < bb ? a : bb, k = a < bb ? bb : a;
+        return (int)(p + packed_index(p, j, k));
+    }
+    const int e2 = e - C::NBLK * 64;
+    const int a = C::col(e2 >> 3, e2 & 7);
+    return a < (int)p ? a : -1;
+}
+
+template <int NB, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
+    using C = SmallP<NB, VEC>;
+    constexpr int U = C::U;
+    extern __shared__ double red[];  // [kWarps][FRAG]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, kk = lane & 3;
+    const uint32_t p = VEC ? 8u * NB : job.p;  // compile-time for the vector layout
+    const uint64_t E = partial_len(p);
+
+    for (uint64_t t = job.tile_begin + blockIdx.x; t < job.tile_end; t += gridDim.x) {
+        const uint32_t r = range_of_tile(job.tile_prefix, job.n_ranges, t);
+        const uint64_t rs = __ldg(job.range_start + r), rc = __ldg(job.range_count + r);
+        const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + r)) * kTileRows;
+        const uint64_t left = rs + rc - row0;
+        const uint32_t rows = left < kTileRows ? (uint32_t)left : kTileRows;
+        const double* __restrict__ tile = job.base + (row0 - job.base_row) * p;
+
+        double c[NB];
+#pragma unroll
+        for (int J = 0; J < NB; ++J) {
+            const int cj = C::col(J, g);
+            c[J] = (job.shift != nullptr && cj < (int)p) ? job.shift[(uint64_t)r * p + cj] : 0.0;
+        }
+        double acc[C::NBLK][2];
+        double s[NB];
+#pragma unroll
+        for (int b = 0; b < C::NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+        for (int J = 0; J < NB; ++J) s[J] = 0.0;
+
+        const uint32_t nks = rows >> 2;
+        const uint32_t kstride = kWarps * 4 * p;  // doubles between a warp's consecutive k-steps
+        uint32_t ks = warp;
+        const double* rowp = tile + (warp * 4 + kk) * p;
+        for (; ks + kWarps * (U - 1) < nks; ks += kWarps * U, rowp += U * kstride) {
+            double x[U][NB];
+#pragma unroll
+            for (int u = 0; u < U; ++u) load_row<NB, VEC>(rowp + u * kstride, g, p, x[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) step<NB>(x[u], c, acc, s);
+        }
+        for (; ks < nks; ks += kWarps, rowp += kstride) {
+            double x[NB];
+            load_row<NB, VEC>(rowp, g, p, x);
+            step<NB>(x, c, acc, s);
+        }
+        // Ragged tail (rows % 4): the warp whose turn k-step nks is; missing rows add 0.
+        if ((rows & 3) && warp == (int)(nks % kWarps)) {
+            const uint32_t row = nks * 4 + kk;
+            double x[NB];
+            if (row < rows) {
+                load_row<NB, VEC>(tile + (uint64_t)row * p, g, p, x);
+            } else {
+#pragma unroll
+                for (int J = 0; J < NB; ++J) x[J] = c[J];
+            }
+            step<NB>(x, c, acc, s);
+        }
+
+        // ---- epilogue: fixed-order reduction to the canonical tile partial ----
+#pragma unroll
+        for (int J = 0; J < NB; ++J) {
+            s[J] += __shfl_xor_sync(0xffffffffu, s[J], 1);
+            s[J] += __shfl_xor_sync(0xffffffffu, s[J], 2);
+        }
+        double* mine = red + warp * C::FRAG;
+#pragma unroll
+        for (int b = 0; b < C::NBLK; ++b) {
+            mine[b * 64 + lane * 2] = acc[b][0];
+            mine[b * 64 + lane * 2 + 1] = acc[b][1];
+        }
+        if (kk == 0) {
+#pragma unroll
+            for (int J = 0; J < NB; ++J) mine[C::NBLK * 64 + J * 8 + g] = s[J];
+        }
+        __syncthreads();
+        double* out = job.tile_partials + t * E;
+        for (int e = threadIdx.x; e < C::FRAG; e += kThreads) {
+            double v = red[e];
+#pragma unroll
+            for (int w = 1; w < kWarps; ++w) v += red[w * C::FRAG + e];
+            const int slot = canonical_slot<NB, VEC>(e, p);
+            if (slot >= 0) out[slot] = v;
+        }
+        __syncthreads();
+    }
+}
+
+template <int NB, bool VEC>
+cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
+    constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, VEC>::FRAG;
+    cudaError_t e = cudaFuncSetAttribute(k_smallp<NB, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp<NB, VEC>, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t tiles = job.tile_end - job.tile_begin;
+    const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
+    if (grid == 0) return cudaSuccess;
+    k_smallp<NB, VEC><<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
+    const uint32_t p = job.p;
+    const int nb = (int)((p + 7) / 8);
+    // 128-bit loads need p a multiple of 16 and a 16-byte aligned base.
+    const bool vec = (p == 8u * nb) && (nb % 2 == 0) && (reinterpret_cast<uintptr_t>(job.base) % 16 == 0);
+    switch (nb) {
+        case 1: return launch_nb<1, false>(job, sms, stream);
+        case 2: return vec ? launch_nb<2, true>(job, sms, stream) : launch_nb<2, false>(job, sms, stream);
+        case 3: return launch_nb<3, false>(job, sms, stream);
+        case 4: return vec ? launch_nb<4, true>(job, sms, stream) : launch_nb<4, false>(job, sms, stream);
+        case 5: return launch_nb<5, false>(job, sms, stream);
+        case 6: return vec ? launch_nb<6, true>(job, sms, stream) : launch_nb<6, false>(job, sms, stream);
+        case 7: return launch_nb<7, false>(job, sms, stream);
+        case 8: return vec ? launch_nb<8, true>(job, sms, stream) : launch_nb<8, false>(job, sms, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sstat_b200

@@ -1,0 +1,53 @@
+// kernels.h — host-callable launchers of the device kernels (all enqueue on `stream`).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace sstat_b200 {
+
+// K1: tiles [job.tile_begin, job.tile_end), p <= 64; persistent grid of
+// min(tiles, sms x resident CTAs per SM).
+cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream);
+
+// K2: tiles for p > 64 (smem-staged DMMA SYRK).
+cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream);
+
+// shift[r][j] = first row of local range r (0 when the range is empty).
+cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uint64_t* range_start,
+                                const uint64_t* range_count, uint32_t n_ranges, uint32_t p, double* shift,
+                                cudaStream_t stream);
+
+// K3a: fold each local range's tile partials in ascending tile order, map the shifted
+// moments back to raw sums / X^T X, write [kHdr + r*E] of `rank_buf`, and flag
+// non-finite ranges (global index first_range + r) in the header.
+cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_prefix, const uint64_t* range_count,
+                              const double* shift, uint32_t n_ranges, uint32_t p, uint64_t first_range,
+                              double* rank_buf, uint32_t* flags, cudaStream_t stream);
+
+// First non-finite value (row-major) over the flagged local ranges (flags[r] != 0);
+// min absolute linear index row*p + col lands in header[1].  No-op when none flagged.
+cudaError_t launch_find_nonfinite(const double* base, uint64_t base_row, const uint64_t* range_start,
+                                  const uint64_t* range_count, uint32_t n_ranges, uint32_t p, const uint32_t* flags,
+                                  double* rank_buf, int grid, cudaStream_t stream);
+
+// K3b: ascending fold over all n_ranges global ranges from +0.0 (reduce.hpp:142-145).
+// Range r lives in rank q = owner(r) at buf + q*rank_stride + kHdr + (r - first(q))*E.
+// precision 1 rounds every add through binary32 (merge_suffstats, suffstats.cpp:92-98).
+cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
+                              uint32_t precision, double* out, cudaStream_t stream);
+
+// Reference-order accumulation: one sequential mul-then-add chain per (range, entry)
+// exactly as accumulate_into<Acc> (suffstats.cpp:56-67); precision 1 = binary32.
+// Writes raw range partials out[r*E] and flags non-finite ranges (flags[r], hdr[0]).
+cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_t* range_start,
+                            const uint64_t* range_count, uint32_t n_ranges, uint32_t p, uint32_t precision,
+                            uint64_t first_range, double* hdr, double* out, uint32_t* flags, cudaStream_t stream);
+
+// K5: synthetic rows [first_row, first_row + n_rows) (bit-identical to the oracle).
+cudaError_t launch_generate(double* dst, uint32_t kind, uint64_t seed, double mu, uint32_t n_int, uint64_t first_row,
+                            uint64_t n_rows, uint32_t p, cudaStream_t stream);
+
+}  // namespace sstat_b200

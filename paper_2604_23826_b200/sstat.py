@@ -1,0 +1,463 @@
+"""Host-side mirror of the reference's sufficient-statistics interface, over the B200 engine.
+
+Names, argument meaning and error behaviour follow the reference
+(paths relative to /root/reference/proj):
+
+  DatasetSchema                   include/sstat/schema.hpp:15-62
+  PrecisionMode, RowRange,
+  Partition, ReductionPlan,
+  ReductionTimings                include/sstat/reduce.hpp:18-60
+  plan_partitions                 src/reduce.cpp:8-16
+  Chunk                           include/sstat/chunk.hpp:13-24
+  SuffStats                       include/sstat/suffstats.hpp:19-30 (cross = SymPacked,
+                                  include/sstat/linalg.hpp:50-81)
+  accumulate_chunk                src/suffstats.cpp:74-84
+  merge_suffstats                 src/suffstats.cpp:86-105
+  dataset_suffstats               src/suffstats.cpp:279-288 (run_reduction,
+                                  include/sstat/reduce.hpp:70-146)
+  Error hierarchy                 include/sstat/errors.hpp:12-94
+
+Every accumulation runs on the GPU through libsstat_b200.so (the C ABI of
+include/sstat_cuda.h).  There is no CPU fallback: without the library or a CUDA
+device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+
+# ---------------------------------------------------------------- errors (errors.hpp)
+class Error(RuntimeError):
+    """Base class for all engine errors (errors.hpp:12-16)."""
+
+
+class IoError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class SchemaMismatchError(Error):
+    pass
+
+
+class NonFiniteError(Error):
+    """Non-finite value; row absolute 0-based, column 0-based (errors.hpp:59-72)."""
+
+    def __init__(self, row: int, column: int, what: str):
+        super().__init__(what)
+        self._row, self._column = row, column
+
+    def row(self) -> int:
+        return self._row
+
+    def column(self) -> int:
+        return self._column
+
+
+class ReductionError(Error):
+    """A per-chunk job failed inside a reduction (errors.hpp:85-92)."""
+
+    def __init__(self, range_index: int, what: str, cause: Optional[Error] = None):
+        super().__init__(what)
+        self._range_index = range_index
+        self.cause = cause
+
+    def range_index(self) -> int:
+        return self._range_index
+
+
+class DeviceError(Error):
+    """CUDA / NCCL / out-of-memory / unsupported: no reference equivalent."""
+
+    def __init__(self, status: int, what: str):
+        super().__init__(what)
+        self.status = status
+
+
+# ---------------------------------------------------------------- plan types (reduce.hpp)
+class PrecisionMode(enum.IntEnum):
+    Binary64 = 0
+    Binary32Diagnostic = 1
+
+
+@dataclass(frozen=True)
+class RowRange:
+    start_row: int = 0
+    row_count: int = 0
+
+
+@dataclass
+class Partition:
+    ranges: List[RowRange] = field(default_factory=list)
+
+    def total_rows(self) -> int:
+        return sum(r.row_count for r in self.ranges)
+
+
+@dataclass
+class ReductionPlan:
+    partition: Partition = field(default_factory=Partition)
+    worker_count: int = 1  # accepted for API parity; the device decides its own parallelism
+    precision: PrecisionMode = PrecisionMode.Binary64
+
+
+@dataclass
+class ReductionTimings:
+    read_seconds: float = 0.0  # host->device copy time (streamed sources)
+    work_seconds: float = 0.0  # accumulate + fold kernels (device events)
+    bytes_read: int = 0
+    exchange_seconds: float = 0.0
+    total_seconds: float = 0.0
+    kernel_launches: int = 0
+
+
+def plan_partitions(n_rows: int, chunk_rows: int) -> Partition:
+    """ceil(n_rows / chunk_rows) ranges (reduce.cpp:8-16); invalid_argument on 0."""
+    if chunk_rows == 0:
+        raise ValueError("plan_partitions: chunk_rows must be >= 1")
+    if n_rows == 0:
+        raise ValueError("plan_partitions: n_rows must be >= 1")
+    return Partition([RowRange(s, min(chunk_rows, n_rows - s)) for s in range(0, n_rows, chunk_rows)])
+
+
+# ---------------------------------------------------------------- schema / stats
+@dataclass
+class DatasetSchema:
+    column_names: List[str] = field(default_factory=list)
+    identifier_columns: List[int] = field(default_factory=list)
+
+    def column_count(self) -> int:
+        return len(self.column_names)
+
+    def is_identifier(self, column: int) -> bool:
+        return column in self.identifier_columns
+
+    def validate(self) -> None:
+        if not self.column_names:
+            raise ValueError("schema: column count must be >= 1")
+        prev = -1
+        for c in self.identifier_columns:
+            if c >= len(self.column_names):
+                raise ValueError("schema: identifier column out of range")
+            if c <= prev:
+                raise ValueError("schema: identifier columns must be sorted and unique")
+            prev = c
+
+    @staticmethod
+    def table1() -> "DatasetSchema":
+        return DatasetSchema(list("ABCDEFGHIJK"), [0])
+
+    @staticmethod
+    def iid_uniform(p: int) -> "DatasetSchema":
+        return DatasetSchema(["A"] + [f"U{i}" for i in range(1, p + 1)], [0])
+
+    @staticmethod
+    def generic(p: int, leading_identifier: bool = True) -> "DatasetSchema":
+        return DatasetSchema([f"c{i}" for i in range(1, p + 1)], [0] if leading_identifier and p > 0 else [])
+
+
+def packed_index(p: int, j: int, k: int) -> int:
+    if j > k:
+        j, k = k, j
+    return j * p - j * (j - 1) // 2 + (k - j)
+
+
+@dataclass
+class SuffStats:
+    n: int
+    sums: np.ndarray  # [p] float64
+    cross: np.ndarray  # [p(p+1)/2] float64, SymPacked order
+    schema: DatasetSchema
+    precision: PrecisionMode = PrecisionMode.Binary64
+
+    @staticmethod
+    def empty(schema: DatasetSchema, precision: PrecisionMode = PrecisionMode.Binary64) -> "SuffStats":
+        schema.validate()
+        p = schema.column_count()
+        return SuffStats(0, np.zeros(p), np.zeros(p * (p + 1) // 2), schema, PrecisionMode(precision))
+
+    def cross_at(self, j: int, k: int) -> float:
+        return float(self.cross[packed_index(len(self.sums), j, k)])
+
+    def cross_full(self) -> np.ndarray:
+        p = len(self.sums)
+        m = np.zeros((p, p))
+        iu = np.triu_indices(p)
+        m[iu] = self.cross
+        m[(iu[1], iu[0])] = self.cross
+        return m
+
+    def __eq__(self, other: object) -> bool:  # the defaulted operator== (value equality)
+        if not isinstance(other, SuffStats):
+            return NotImplemented
+        return (
+            self.n == other.n
+            and self.schema == other.schema
+            and self.precision == other.precision
+            and np.array_equal(self.sums, other.sums)
+            and np.array_equal(self.cross, other.cross)
+        )
+
+    def bit_equal(self, other: "SuffStats") -> bool:
+        return (
+            self.n == other.n
+            and np.array_equal(self.sums.view(np.uint64), other.sums.view(np.uint64))
+            and np.array_equal(self.cross.view(np.uint64), other.cross.view(np.uint64))
+        )
+
+
+@dataclass
+class Chunk:
+    """Row-major block of rows (chunk.hpp:13-24); values: numpy array or torch tensor."""
+
+    start_row: int
+    row_count: int
+    column_count: int
+    values: object
+
+
+def merge_suffstats(a: SuffStats, b: SuffStats) -> SuffStats:
+    """Elementwise merge (suffstats.cpp:86-105) via the library's host merge."""
+    if a.schema != b.schema:
+        raise SchemaMismatchError("merge_suffstats: schemas differ")
+    if a.precision != b.precision:
+        raise SchemaMismatchError("merge_suffstats: precision modes differ")
+    lib = N.load()
+    n = ctypes.c_uint64(a.n)
+    sums = np.ascontiguousarray(a.sums, dtype=np.float64).copy()
+    cross = np.ascontiguousarray(a.cross, dtype=np.float64).copy()
+    bs = np.ascontiguousarray(b.sums, dtype=np.float64)
+    bc = np.ascontiguousarray(b.cross, dtype=np.float64)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib.sstat_merge(len(sums), int(a.precision), ctypes.byref(n), sums.ctypes.data_as(dp), cross.ctypes.data_as(dp),
+                         b.n, bs.ctypes.data_as(dp), bc.ctypes.data_as(dp))
+    if st != N.OK:
+        raise ValueError(N.status_string(st))
+    return SuffStats(n.value, sums, cross, a.schema, a.precision)
+
+
+# ---------------------------------------------------------------- the engine
+def _raise(status: int, err: N.Error, in_dataset: bool) -> None:
+    msg = err.msg.decode(errors="replace")
+    if status == N.ERR_NONFINITE:
+        nf = NonFiniteError(err.row, err.col, f"non-finite value at row {err.row}, column {err.col}")
+        if in_dataset:
+            raise ReductionError(err.range_index, msg, nf)
+        raise nf
+    if status == N.ERR_SCHEMA:
+        if in_dataset and msg.startswith("range "):
+            raise ReductionError(err.range_index, msg, SchemaMismatchError(msg))
+        raise SchemaMismatchError(msg)
+    if status == N.ERR_INVALID:
+        raise ValueError(msg)
+    if status == N.ERR_IO:
+        raise IoError(msg)
+    if status == N.ERR_FORMAT:
+        raise FormatError(msg)
+    raise DeviceError(status, f"{N.status_string(status)}: {msg}")
+
+
+def _is_torch_cuda(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+class Engine:
+    """One CUDA context of the B200 engine (sstat_cuda_ctx), bound to one device."""
+
+    def __init__(self, device: Optional[int] = None):
+        self._lib = N.load()
+        self._ctx = ctypes.c_void_p()
+        st = self._lib.sstat_cuda_init(ctypes.byref(self._ctx), -1 if device is None else int(device))
+        if st != N.OK:
+            raise DeviceError(st, f"sstat_cuda_init failed: {N.status_string(st)}")
+        self.rank, self.world = 0, 1
+
+    def close(self) -> None:
+        if self._ctx:
+            self._lib.sstat_cuda_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- configuration
+    def set_stream(self, cuda_stream: int) -> None:
+        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(self._lib.sstat_cuda_set_stream(self._ctx, ctypes.c_void_p(cuda_stream or None)))
+
+    def set_staging(self, slots: int, slot_bytes: int) -> None:
+        self._check(self._lib.sstat_cuda_set_staging(self._ctx, slots, slot_bytes))
+
+    def init_distributed(self, rank: int, world: int, unique_id: Optional[bytes]) -> None:
+        """Attach an NCCL communicator (one process per GPU)."""
+        buf = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+        self._check(self._lib.sstat_cuda_comm_init(self._ctx, rank, world, buf, 128 if buf is not None else 0))
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = N.load()
+        buf = ctypes.create_string_buffer(128)
+        st = lib.sstat_cuda_nccl_unique_id(buf, 128)
+        if st != N.OK:
+            raise DeviceError(st, "ncclGetUniqueId failed")
+        return buf.raw
+
+    def _check(self, st: int) -> None:
+        if st != N.OK:
+            raise DeviceError(st, N.status_string(st))
+
+    # -- hot path
+    def accumulate_chunk(self, chunk: Chunk, schema: DatasetSchema,
+                         precision: PrecisionMode = PrecisionMode.Binary64, flags: int = 0) -> SuffStats:
+        """accumulate_chunk (suffstats.cpp:74-84) on a host or device chunk."""
+        schema.validate()
+        p = schema.column_count()
+        if chunk.column_count != p:
+            raise SchemaMismatchError(f"chunk has {chunk.column_count} columns, schema has {p}")
+        ptr, keep = self._rows_pointer(chunk.values, chunk.row_count * p)
+        out = SuffStats.empty(schema, precision)
+        n = ctypes.c_uint64()
+        err = N.Error()
+        dp = ctypes.POINTER(ctypes.c_double)
+        st = self._lib.sstat_cuda_accumulate(self._ctx, ptr, chunk.row_count, p, chunk.start_row, int(precision), flags,
+                                             ctypes.byref(n), out.sums.ctypes.data_as(dp),
+                                             out.cross.ctypes.data_as(dp), ctypes.byref(err))
+        del keep
+        if st != N.OK:
+            _raise(st, err, in_dataset=False)
+        out.n = n.value
+        return out
+
+    def dataset_suffstats(self, dataset, schema: DatasetSchema, plan: ReductionPlan,
+                          timings: Optional[ReductionTimings] = None, flags: int = 0,
+                          first_row: int = 0, n_rows: Optional[int] = None) -> SuffStats:
+        """dataset_suffstats (suffstats.cpp:279-288).
+
+        dataset: an SSTATBIN path, a CUDA tensor (HBM-resident rows), or a host array
+        (numpy / CPU tensor; pinned memory is copied by DMA).  With a communicator,
+        each rank passes its shard and ``first_row`` = the absolute index of its row 0.
+        """
+        schema.validate()
+        p = schema.column_count()
+        src = N.Source()
+        keep = None
+        if isinstance(dataset, (str, os.PathLike)):
+            src.kind = N.SRC_FILE
+            keep = os.fsencode(os.fspath(dataset))
+            src.path = keep
+        else:
+            ptr, keep = self._rows_pointer(dataset, None)
+            src.kind = N.SRC_DEVICE if _is_torch_cuda(dataset) else N.SRC_HOST
+            src.ptr = ptr
+            rows = n_rows if n_rows is not None else _rows_of(dataset, p)
+            src.first_row = first_row
+            src.n_rows = rows
+        R = len(plan.partition.ranges)
+        starts = np.array([r.start_row for r in plan.partition.ranges], dtype=np.uint64)
+        counts = np.array([r.row_count for r in plan.partition.ranges], dtype=np.uint64)
+        out = SuffStats.empty(schema, plan.precision)
+        n = ctypes.c_uint64()
+        err = N.Error()
+        tm = N.Timings()
+        dp = ctypes.POINTER(ctypes.c_double)
+        st = self._lib.sstat_cuda_dataset(self._ctx, ctypes.byref(src), p, starts.ctypes.data, counts.ctypes.data, R,
+                                          int(plan.precision), flags, ctypes.byref(n), out.sums.ctypes.data_as(dp),
+                                          out.cross.ctypes.data_as(dp), ctypes.byref(tm), ctypes.byref(err))
+        del keep
+        if st != N.OK:
+            _raise(st, err, in_dataset=True)
+        out.n = n.value
+        if timings is not None:
+            timings.read_seconds = tm.h2d_seconds
+            timings.work_seconds = tm.kernel_seconds + tm.fold_seconds
+            timings.bytes_read = tm.bytes_read
+            timings.exchange_seconds = tm.exchange_seconds
+            timings.total_seconds = tm.total_seconds
+            timings.kernel_launches = tm.kernel_launches
+        self.last_timings = tm
+        return out
+
+    def generate(self, dst, kind: int, seed: int, mu: float, n_int: int, first_row: int, n_rows: int, p: int) -> None:
+        """Fill a CUDA tensor with synthetic rows (bit-identical to oracle_generate)."""
+        if not _is_torch_cuda(dst):
+            raise TypeError("generate needs a CUDA tensor")
+        self._check(self._lib.sstat_cuda_generate(self._ctx, ctypes.c_void_p(dst.data_ptr()), kind, seed, mu, n_int,
+                                                  first_row, n_rows, p))
+
+    # -- helpers
+    @staticmethod
+    def _rows_pointer(values, expect: Optional[int]):
+        if type(values).__module__.startswith("torch"):
+            import torch
+
+            if values.dtype != torch.float64:
+                raise TypeError("rows must be float64")
+            if not values.is_contiguous():
+                raise ValueError("rows must be contiguous row-major")
+            if expect is not None and values.numel() != expect:
+                raise ValueError("chunk values size does not match row_count * column_count")
+            return ctypes.c_void_p(values.data_ptr() or None), values
+        arr = np.ascontiguousarray(values, dtype=np.float64)
+        if expect is not None and arr.size != expect:
+            raise ValueError("chunk values size does not match row_count * column_count")
+        return ctypes.c_void_p(arr.ctypes.data if arr.size else None), arr
+
+
+def _rows_of(dataset, p: int) -> int:
+    numel = dataset.numel() if hasattr(dataset, "numel") else np.asarray(dataset).size
+    return int(numel) // p
+
+
+_default = {}
+_default_lock = threading.Lock()
+
+
+def default_engine(device: Optional[int] = None) -> Engine:
+    """Process-wide engine per device (like the reference's free functions)."""
+    if device is None:
+        try:
+            import torch
+
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        except Exception:  # pragma: no cover
+            device = 0
+    with _default_lock:
+        if device not in _default:
+            _default[device] = Engine(device)
+        return _default[device]
+
+
+def accumulate_chunk(chunk: Chunk, schema: DatasetSchema,
+                     precision: PrecisionMode = PrecisionMode.Binary64) -> SuffStats:
+    return default_engine().accumulate_chunk(chunk, schema, precision)
+
+
+def dataset_suffstats(dataset, schema: DatasetSchema, plan: ReductionPlan,
+                      timings: Optional[ReductionTimings] = None) -> SuffStats:
+    return default_engine().dataset_suffstats(dataset, schema, plan, timings)
+
+
+def shard_ranges(n_ranges: int, rank: int, world: int):
+    """Ranges [first, last) owned by `rank` (contiguous row shards, floor split)."""
+    lib = N.load()
+    f, l = ctypes.c_uint64(), ctypes.c_uint64()
+    st = lib.sstat_shard_ranges(n_ranges, rank, world, ctypes.byref(f), ctypes.byref(l))
+    if st != N.OK:
+        raise ValueError(N.status_string(st))
+    return f.value, l.value

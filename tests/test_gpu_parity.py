@@ -1,0 +1,368 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own results.
+
+Bars (BASELINE.json north_star):
+  * counts: exact; integer-valued columns: bit-exact (all partial sums < 2^53);
+  * FP64 sums / X^T X: Cauchy-Schwarz-normalised error <= 1e-12
+        |dS_jk| <= 1e-12 sqrt(S_jj S_kk),  |ds_j| <= 1e-12 sqrt(n S_jj);
+  * covariance (CS-normalised) and correlation (absolute) <= 1e-12, eigenvalues 1e-10 relative;
+  * SSTAT_FLAG_REFEXACT (and Binary32Diagnostic): bit-identical to the reference for any data.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits, cs_err, sums_err, unhex
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def torch_mod():
+    import torch
+
+    return torch
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def schema(p, ids=()):
+    from paper_2604_23826_b200 import DatasetSchema
+
+    s = DatasetSchema.generic(p, False)
+    s.identifier_columns = list(ids)
+    return s
+
+
+def plan(n, chunk, precision=0):
+    from paper_2604_23826_b200 import PrecisionMode, ReductionPlan, plan_partitions
+
+    return ReductionPlan(plan_partitions(n, chunk), 1, PrecisionMode(precision))
+
+
+def to_dev(X):
+    torch = torch_mod()
+    return torch.from_numpy(np.ascontiguousarray(X)).cuda()
+
+
+def integer_pairs(X):
+    """(j,k) packed indices whose columns are integer-valued, and integral column ids."""
+    p = X.shape[1]
+    integral = [j for j in range(p) if np.all(X[:, j] == np.trunc(X[:, j]))]
+    idx = [j * p - j * (j - 1) // 2 + (k - j) for j in integral for k in integral if k >= j]
+    return integral, np.array(sorted(idx), dtype=np.int64)
+
+
+def check_against(got, n, sums, cross, X=None, tol=TOL):
+    p = len(sums)
+    assert got.n == n
+    assert cs_err(got.cross, cross, p) <= tol
+    assert sums_err(got.sums, sums, cross, n, p) <= tol
+    if X is not None:
+        integral, idx = integer_pairs(X)
+        if integral:
+            assert np.array_equal(bits(got.sums[integral]), bits(sums[integral]))
+        if idx.size:
+            assert np.array_equal(bits(got.cross[idx]), bits(cross[idx]))
+
+
+# ----------------------------------------------------------------- known answers
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_kats(engine, golden, where):
+    from paper_2604_23826_b200 import Chunk, NonFiniteError
+
+    for name in ("single_row", "orthogonal"):
+        c = golden[name]
+        X = np.array(c["rows"], dtype=np.float64)
+        vals = X if where == "host" else to_dev(X)
+        for flags in (0, 2):
+            ss = engine.accumulate_chunk(Chunk(0, X.shape[0], 2, vals), schema(2), flags=flags)
+            assert ss.n == c["n"]
+            assert np.array_equal(bits(ss.sums), bits(unhex(c["sums"])))
+            assert np.array_equal(bits(ss.cross), bits(unhex(c["cross"])))
+    bad = np.array([[1.0, 2.0], [3.0, np.inf]])
+    vals = bad if where == "host" else to_dev(bad)
+    with pytest.raises(NonFiniteError) as ei:
+        engine.accumulate_chunk(Chunk(40, 2, 2, vals), schema(2))
+    assert (ei.value.row(), ei.value.column()) == (41, 1)
+    assert str(ei.value) == golden["nonfinite_chunk"]["error"]["msg"]
+
+
+def test_empty_chunk_and_schema_mismatch(engine):
+    from paper_2604_23826_b200 import Chunk, SchemaMismatchError
+
+    ss = engine.accumulate_chunk(Chunk(0, 0, 3, np.zeros(0)), schema(3))
+    assert ss.n == 0 and not ss.sums.any() and not ss.cross.any()
+    with pytest.raises(SchemaMismatchError):
+        engine.accumulate_chunk(Chunk(0, 1, 2, np.zeros(2)), schema(3))
+
+
+def test_cauchy_schwarz_random_chunks(engine):
+    """test_suffstats.cpp:130-146 on the GPU path."""
+    from paper_2604_23826_b200 import Chunk
+
+    rng = np.random.default_rng(77)
+    for _ in range(20):
+        X = rng.normal(0.0, 3.0, size=(200, 5))
+        ss = engine.accumulate_chunk(Chunk(0, 200, 5, X), schema(5))
+        S = ss.cross_full()
+        for j in range(5):
+            for k in range(j + 1, 5):
+                assert S[j, k] ** 2 <= S[j, j] * S[k, k] * (1 + 4e-16)
+
+
+def test_table1_accumulate(engine, oracle, golden):
+    from paper_2604_23826_b200 import Chunk, PrecisionMode
+
+    c = golden["table1_seed21"]
+    X = oracle.table1_chunk(21, 1, 10000)
+    assert sha(X) == c["input_sha256"]
+    ref_s, ref_S = unhex(c["sums"]), unhex(c["cross"])
+    for vals in (X, to_dev(X)):
+        fast = engine.accumulate_chunk(Chunk(0, 10000, 11, vals), schema(11, [0]))
+        check_against(fast, 10000, ref_s, ref_S, X)
+        exact = engine.accumulate_chunk(Chunk(0, 10000, 11, vals), schema(11, [0]), flags=2)
+        assert np.array_equal(bits(exact.sums), bits(ref_s)) and np.array_equal(bits(exact.cross), bits(ref_S))
+    c32 = golden["table1_seed21_binary32"]
+    f32 = engine.accumulate_chunk(Chunk(0, 10000, 11, X), schema(11, [0]), PrecisionMode.Binary32Diagnostic)
+    assert np.array_equal(bits(f32.cross), bits(unhex(c32["cross"])))
+    assert np.array_equal(bits(f32.sums), bits(unhex(c32["sums"])))
+
+
+def test_table1_dataset_every_source(engine, oracle, reference, golden, tmp_path):
+    """test_suffstats.cpp:100-128: Table1 seed 5, 20,000 rows, chunk 1024."""
+    torch = torch_mod()
+    c = golden["table1_seed5_dataset"]
+    X = oracle.table1_chunk(5, 1, 20000)
+    ref_s, ref_S = unhex(c["sums"]), unhex(c["cross"])
+    f = tmp_path / "t5.bin"
+    reference.write_binary(str(f), X, 11)
+    pinned = torch.from_numpy(X.copy()).pin_memory()
+    sources = {"device": to_dev(X), "host": X, "pinned": pinned, "file": str(f)}
+    fast = {}
+    for name, src in sources.items():
+        got = engine.dataset_suffstats(src, schema(11, [0]), plan(20000, 1024))
+        check_against(got, 20000, ref_s, ref_S, X)
+        fast[name] = got
+        exact = engine.dataset_suffstats(src, schema(11, [0]), plan(20000, 1024), flags=2)
+        assert np.array_equal(bits(exact.sums), bits(ref_s)) and np.array_equal(bits(exact.cross), bits(ref_S))
+    # the fast result is a fixed function of (data, plan): identical for every source
+    for name in ("host", "pinned", "file"):
+        assert fast[name].bit_equal(fast["device"]), name
+
+
+GEN_CASES = ["c1_small", "c2_small", "c2_mu0", "ragged_p5", "p24", "p64"]
+
+
+@pytest.mark.parametrize("name", GEN_CASES)
+def test_generated_cases(engine, oracle, reference, golden, name):
+    torch = torch_mod()
+    c = golden[name]
+    g = c["gen"]
+    X = oracle.generate(g["kind"], g["seed"], g["mu"], g["n_int"], 0, g["n"], g["p"])
+    D = torch.empty((g["n"], g["p"]), dtype=torch.float64, device="cuda")
+    engine.generate(D, g["kind"], g["seed"], g["mu"], g["n_int"], 0, g["n"], g["p"])
+    assert sha(D.cpu().numpy()) == c["input_sha256"], "GPU generator is not bit-identical to the oracle"
+    ids = [0] if g["kind"] == 1 else []
+    ref_s, ref_S = unhex(c["sums"]), unhex(c["cross"])
+    for flags in (0, 1):  # with and without the per-range shift
+        got = engine.dataset_suffstats(D, schema(g["p"], ids), plan(g["n"], g["chunk"]), flags=flags)
+        check_against(got, c["n"], ref_s, ref_S, X)
+    exact = engine.dataset_suffstats(D, schema(g["p"], ids), plan(g["n"], g["chunk"]), flags=2)
+    assert np.array_equal(bits(exact.sums), bits(ref_s)) and np.array_equal(bits(exact.cross), bits(ref_S))
+    # downstream (host finalisation of the reference, unchanged) on the GPU SuffStats
+    got = engine.dataset_suffstats(D, schema(g["p"], ids), plan(g["n"], g["chunk"]))
+    mean, cov, corr = reference.analyze(g["p"], ids, got.n, got.sums, got.cross)
+    an = c["analysis"]
+    q = mean.size
+    iu = np.triu_indices(q)
+    rcov = np.zeros((q, q))
+    rcov[iu] = unhex(an["cov_upper"])
+    rcov = rcov + np.triu(rcov, 1).T
+    d = np.sqrt(np.outer(np.diag(rcov), np.diag(rcov)))
+    assert np.max(np.abs(cov - rcov) / d) <= TOL
+    rcorr = np.zeros((q, q))
+    rcorr[iu] = unhex(an["corr_upper"])
+    rcorr = rcorr + np.triu(rcorr, 1).T
+    assert np.max(np.abs(corr - rcorr)) <= TOL
+    for basis, key in ((1, "pca_corr_eigenvalues"), (0, "pca_cov_eigenvalues")):
+        ev = reference.run_pca(g["p"], ids, got.n, got.sums, got.cross, basis=basis)
+        rev = unhex(c[key])
+        assert np.max(np.abs(ev - rev) / np.abs(rev)) <= 1e-10
+
+
+def test_dataset_nonfinite(engine, oracle, golden, tmp_path, reference):
+    from paper_2604_23826_b200 import NonFiniteError, ReductionError
+
+    c = golden["dataset_nonfinite"]
+    g = c["gen"]
+    X = oracle.generate(g["kind"], g["seed"], g["mu"], g["n_int"], 0, g["n"], g["p"])
+    for r, col, kind in c["poison"]:
+        X[r, col] = np.inf if kind == "inf" else np.nan
+    f = tmp_path / "nf.bin"
+    reference.write_binary(str(f), X, 16)
+    for src in (to_dev(X), X, str(f)):
+        for flags in (0, 2):
+            with pytest.raises(ReductionError) as ei:
+                engine.dataset_suffstats(src, schema(16), plan(g["n"], g["chunk"]), flags=flags)
+            assert ei.value.range_index() == c["error"]["range_index"]
+            assert str(ei.value) == c["error"]["msg"]
+            assert isinstance(ei.value.cause, NonFiniteError)
+
+
+def test_overflow_is_not_an_error(engine):
+    """Huge finite values overflow the sums to inf without a non-finite input: no error."""
+    X = np.full((64, 3), 1e300)
+    got = engine.dataset_suffstats(X, schema(3), plan(64, 16))
+    assert np.isinf(got.cross[0])
+
+
+def test_plan_and_file_errors(engine, oracle, reference, tmp_path):
+    from paper_2604_23826_b200 import FormatError, IoError, ReductionError, SchemaMismatchError
+
+    X = oracle.generate(0, 1, 1.0, 2, 0, 100, 4)
+    with pytest.raises(ValueError, match="partition covers 99 rows"):
+        engine.dataset_suffstats(to_dev(X), schema(4), plan(99, 10))
+    f = tmp_path / "x.bin"
+    reference.write_binary(str(f), X, 4)
+    with pytest.raises(ValueError, match="partition covers 99 rows but dataset has 100"):
+        engine.dataset_suffstats(str(f), schema(4), plan(99, 10))
+    with pytest.raises(ReductionError) as ei:
+        engine.dataset_suffstats(str(f), schema(3), plan(100, 10))
+    assert isinstance(ei.value.cause, SchemaMismatchError) and ei.value.range_index() == 0
+    with pytest.raises(IoError):
+        engine.dataset_suffstats(str(tmp_path / "missing.bin"), schema(4), plan(100, 10))
+    raw = bytearray(f.read_bytes())
+    raw[2] ^= 0xFF
+    (tmp_path / "bad.bin").write_bytes(bytes(raw))
+    with pytest.raises(FormatError):
+        engine.dataset_suffstats(str(tmp_path / "bad.bin"), schema(4), plan(100, 10))
+    (tmp_path / "short.bin").write_bytes(f.read_bytes()[:-8])
+    with pytest.raises(FormatError):
+        engine.dataset_suffstats(str(tmp_path / "short.bin"), schema(4), plan(100, 10))
+
+
+@pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
+def test_sharded_partials_fold_bit_identical(engine, oracle, W):
+    """Row shards per rank (each source holds only its rows) + the rank-ordered fold give the
+    single-device result bit-for-bit: the multi-GPU path minus the NCCL copy."""
+    import ctypes
+
+    from paper_2604_23826_b200 import _native as N
+    from paper_2604_23826_b200 import shard_ranges
+
+    torch = torch_mod()
+    n, p, chunk = 300007, 16, 4099
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 0, 42, 1.0, 2, 0, n, p)
+    pl = plan(n, chunk)
+    whole = engine.dataset_suffstats(D, schema(p), pl)
+    R = len(pl.partition.ranges)
+    starts = np.array([r.start_row for r in pl.partition.ranges], dtype=np.uint64)
+    counts = np.array([r.row_count for r in pl.partition.ranges], dtype=np.uint64)
+    E = p + p * (p + 1) // 2
+    lmax = (R + W - 1) // W
+    stride = 4 + lmax * E
+    buf = np.zeros(W * stride)
+    lib = N.load()
+    for q in range(W):
+        f, l = shard_ranges(R, q, W)
+        r0 = int(starts[f])
+        r1 = int(starts[l - 1] + counts[l - 1])
+        shard = D[r0:r1].contiguous()
+        src = N.Source(kind=N.SRC_DEVICE, ptr=shard.data_ptr(), first_row=r0, n_rows=r1 - r0)
+        out = np.zeros((l - f) * E)
+        err = N.Error()
+        dp = ctypes.POINTER(ctypes.c_double)
+        st = lib.sstat_cuda_range_partials(engine._ctx, ctypes.byref(src), p, starts.ctypes.data, counts.ctypes.data, R,
+                                           f, l, 0, 0, out.ctypes.data_as(dp), ctypes.byref(err))
+        assert st == 0, err.msg
+        buf[q * stride + 4: q * stride + 4 + out.size] = out
+    res = np.zeros(E)
+    dp = ctypes.POINTER(ctypes.c_double)
+    assert lib.sstat_fold_ranges_host(buf.ctypes.data_as(dp), stride, R, W, p, 0, res.ctypes.data_as(dp)) == 0
+    assert np.array_equal(bits(res[:p]), bits(whole.sums))
+    assert np.array_equal(bits(res[p:]), bits(whole.cross))
+
+
+def test_nccl_world1_identical(oracle):
+    """The NCCL exchange path with a communicator of one rank."""
+    from paper_2604_23826_b200 import Engine
+
+    torch = torch_mod()
+    e = Engine(0)
+    uid = Engine.nccl_unique_id()
+    e.init_distributed(0, 1, uid)
+    n, p = 100000, 16
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    e.generate(D, 0, 3, 1.0, 2, 0, n, p)
+    a = e.dataset_suffstats(D, schema(p), plan(n, 8192))
+    e2 = Engine(0)
+    b = e2.dataset_suffstats(D, schema(p), plan(n, 8192))
+    assert a.bit_equal(b)
+    e.close()
+    e2.close()
+
+
+def test_streaming_small_slots_bit_identical(engine, oracle):
+    """Host sources stream through the staging ring; tiny slots force many chunks."""
+    from paper_2604_23826_b200 import Engine
+
+    torch = torch_mod()
+    n, p = 1 << 20, 16
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 0, 5, 1.0, 2, 0, n, p)
+    H = D.cpu()
+    dev = engine.dataset_suffstats(D, schema(p), plan(n, 100003))
+    e = Engine(0)
+    e.set_staging(3, 1 << 20)
+    assert e.dataset_suffstats(H.numpy(), schema(p), plan(n, 100003)).bit_equal(dev)
+    assert e.dataset_suffstats(H.pin_memory(), schema(p), plan(n, 100003)).bit_equal(dev)
+    e.close()
+
+
+def test_c1_full_size(engine, oracle):
+    """Config 1: 1e6 x (8 + ID), the ID column excluded downstream, vs the oracle."""
+    torch = torch_mod()
+    n, p = 1_000_000, 9
+    X = oracle.generate(1, 42, 1.0, 0, 0, n, p)
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 1, 42, 1.0, 0, 0, n, p)
+    assert np.array_equal(bits(D.cpu().numpy()), bits(X))
+    s, c = oracle.plan_partitions(n, 1 << 20)
+    want = oracle.run_reduction(X, p, s, c, 8)
+    got = engine.dataset_suffstats(D, schema(p, [0]), plan(n, 1 << 20))
+    assert got.sums[0] == want[1][0] == n * (n + 1) / 2  # identifier sum, exact
+    check_against(got, n, want[1], want[2])
+
+
+def test_c2_full_size_properties(engine):
+    """Config 2 at full size (1e8 x 16, HBM-resident): fast vs the reference-order mode
+    (bit-identical to the reference by construction) — integer block bit-exact, the rest
+    within tolerance; covariance near the generator's known tridiagonal Sigma."""
+    torch = torch_mod()
+    n, p = 100_000_000, 16
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 0, 42, 1.0, 2, 0, n, p)
+    pl = plan(n, 1 << 20)
+    fast = engine.dataset_suffstats(D, schema(p), pl)
+    exact = engine.dataset_suffstats(D, schema(p), pl, flags=2)
+    assert fast.n == exact.n == n
+    idx = [0, 1, p]  # (0,0), (0,1), (1,1)
+    assert np.array_equal(bits(fast.cross[idx]), bits(exact.cross[idx]))
+    assert np.array_equal(bits(fast.sums[:2]), bits(exact.sums[:2]))
+    assert cs_err(fast.cross, exact.cross, p) <= TOL
+    assert sums_err(fast.sums, exact.sums, exact.cross, n, p) <= TOL
+    mu = fast.sums / n
+    cov = fast.cross_full() / n - np.outer(mu, mu)
+    g = cov[2:, 2:]
+    want = np.diag([1.0] + [1.25] * 13) + np.diag([0.5] * 13, 1) + np.diag([0.5] * 13, -1)
+    assert np.max(np.abs(g - want)) < 2e-3
+    del D
+    torch.cuda.empty_cache()
