@@ -78,10 +78,17 @@ __host__ __device__ inline double fold_entry(const double* buf, uint64_t rank_st
     for (int q = 0; q < world; ++q) {
         const uint64_t f = (uint64_t)q * n_ranges / world, l = (uint64_t)(q + 1) * n_ranges / world;
         const double* part = buf + (uint64_t)q * rank_stride + kHdr + e;
+        const uint64_t cnt = l - f;
         if (precision == 1) {
-            for (uint64_t r = 0; r < l - f; ++r) acc = (double)((float)acc + (float)part[r * E]);
+            for (uint64_t r = 0; r < cnt; ++r) acc = (double)((float)acc + (float)part[r * E]);
         } else {
-            for (uint64_t r = 0; r < l - f; ++r) acc += part[r * E];
+            uint64_t r = 0;
+            for (; r + 8 <= cnt; r += 8) {  // 8 loads in flight, adds stay in range order
+                double v[8];
+                for (int u = 0; u < 8; ++u) v[u] = part[(r + u) * E];
+                for (int u = 0; u < 8; ++u) acc += v[u];
+            }
+            for (; r < cnt; ++r) acc += part[r * E];
         }
     }
     return acc;

@@ -14,13 +14,15 @@ __device__ __forceinline__ bool finite64(double v) { return isfinite(v); }
 
 // Inverse of packed_index: (j, k) with j <= k for packed position i.
 __device__ __forceinline__ void unpack_index(uint32_t p, uint32_t i, uint32_t& j, uint32_t& k) {
-    uint32_t row = 0, start = 0;
-    while (start + (p - row) <= i) {
-        start += p - row;
-        ++row;
-    }
-    j = row;
-    k = row + (i - start);
+    // row j: start(j) = j*p - j(j-1)/2 <= i < start(j+1); estimate then correct
+    const double b = 2.0 * p + 1.0;
+    int64_t row = (int64_t)floor((b - sqrt(b * b - 8.0 * i)) * 0.5);
+    if (row < 0) row = 0;
+    auto start = [p](int64_t jj) { return jj * (int64_t)p - jj * (jj - 1) / 2; };
+    while (row > 0 && start(row) > (int64_t)i) --row;
+    while (row + 1 < (int64_t)p && start(row + 1) <= (int64_t)i) ++row;
+    j = (uint32_t)row;
+    k = (uint32_t)(row + ((int64_t)i - start(row)));
 }
 
 __global__ void k_gather_shift(const double* __restrict__ base, uint64_t base_row, const uint64_t* __restrict__ range_start,
@@ -31,52 +33,74 @@ __global__ void k_gather_shift(const double* __restrict__ base, uint64_t base_ro
     shift[i] = range_count[r] ? base[(range_start[r] - base_row) * p + j] : 0.0;
 }
 
-// One block per local range.  Shifted moments of the range (sum of its tiles, ascending)
-// are mapped back to raw moments with c = shift row, n = range rows:
+// Lane q of kFoldLanes sums tiles t0+q, t0+q+kFoldLanes, ... of entry e (8 loads in flight).
+constexpr int kFoldLanes = 8;
+
+__device__ __forceinline__ double fold_tiles_lane(const double* __restrict__ tp, uint64_t E, uint64_t e, uint64_t t0,
+                                                  uint64_t t1, int q) {
+    double s = 0.0;
+    uint64_t t = t0 + q;
+    for (; t + 7 * kFoldLanes < t1; t += 8 * kFoldLanes) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = tp[(t + u * kFoldLanes) * E + e];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; t < t1; t += kFoldLanes) s += tp[t * E + e];
+    return s;
+}
+
+// One block (8 warps) per local range.  Tile partials of the range are summed in a fixed
+// order (8 interleaved lanes, then lane 0..7), and the shifted moments are mapped back to
+// raw moments with c = shift row, n = range rows:
 //   s_j  = s'_j + n c_j
 //   S_jk = S'_jk + c_j s'_k + c_k s'_j + n c_j c_k
 // (exact for integer data below 2^53, like the reference's own sums).
-__global__ void k_range_fold(const double* __restrict__ tp, const uint64_t* __restrict__ tile_prefix,
-                             const uint64_t* __restrict__ range_count, const double* __restrict__ shift, uint32_t p,
-                             uint64_t first_range, double* rank_buf, uint32_t* flags) {
-    extern __shared__ double sm[];  // [p] shifted sums, [p] shift
+__global__ void __launch_bounds__(256) k_range_fold(const double* __restrict__ tp,
+                                                    const uint64_t* __restrict__ tile_prefix,
+                                                    const uint64_t* __restrict__ range_count,
+                                                    const double* __restrict__ shift, uint32_t p,
+                                                    uint64_t first_range, double* rank_buf, uint32_t* flags) {
+    extern __shared__ double sm[];  // [p] shifted sums, [p] shift, [kFoldLanes][32] lane partials
+    double* ssum = sm;
+    double* sc = sm + p;
+    double* lanes = sm + 2 * p;
     const uint32_t r = blockIdx.x;
     const uint64_t E = partial_len(p);
     const uint64_t t0 = tile_prefix[r], t1 = tile_prefix[r + 1];
     const double n = (double)range_count[r];
     double* out = rank_buf + kHdr + (uint64_t)r * E;
-    for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) {
-        double s = 0.0;
-        for (uint64_t t = t0; t < t1; ++t) s += tp[t * E + j];
-        const double cj = shift ? shift[(uint64_t)r * p + j] : 0.0;
-        sm[j] = s;
-        sm[p + j] = cj;
-        out[j] = s + n * cj;
-        if (!finite64(s) || !finite64(cj)) {
-            flags[r] = 1;
-            atomicMin(reinterpret_cast<ull*>(rank_buf), (ull)(first_range + r));
-        }
-    }
-    __syncthreads();
-    for (uint32_t j = 0; j < p; ++j) {
-        const double sj = sm[j], cj = sm[p + j], ncj = n * cj;
-        for (uint32_t k = j + threadIdx.x; k < p; k += blockDim.x) {
-            const uint64_t e = p + packed_index(p, j, k);
-            double S = 0.0;
-            uint64_t t = t0;
-            for (; t + 4 <= t1; t += 4) {
-                const double a = tp[t * E + e], b = tp[(t + 1) * E + e], c = tp[(t + 2) * E + e], d = tp[(t + 3) * E + e];
-                S += a;
-                S += b;
-                S += c;
-                S += d;
+    const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
+    for (int phase = 0; phase < 2; ++phase) {
+        const uint64_t lo = phase == 0 ? 0 : p, hi = phase == 0 ? p : E;
+        for (uint64_t e0 = lo; e0 < hi; e0 += 32) {
+            const uint64_t e = e0 + le;
+            lanes[q * 32 + le] = e < hi ? fold_tiles_lane(tp, E, e, t0, t1, q) : 0.0;
+            __syncthreads();
+            if (q == 0 && e < hi) {
+                double S = lanes[le];
+#pragma unroll
+                for (int w = 1; w < kFoldLanes; ++w) S += lanes[w * 32 + le];
+                if (phase == 0) {
+                    const double cj = shift ? shift[(uint64_t)r * p + e] : 0.0;
+                    ssum[e] = S;
+                    sc[e] = cj;
+                    out[e] = S + n * cj;
+                    if (!finite64(S) || !finite64(cj)) {
+                        flags[r] = 1;
+                        atomicMin(reinterpret_cast<ull*>(rank_buf), (ull)(first_range + r));
+                    }
+                } else {
+                    if (shift) {
+                        uint32_t j, k;
+                        unpack_index(p, (uint32_t)(e - p), j, k);
+                        S = ((S + sc[j] * ssum[k]) + sc[k] * ssum[j]) + (n * sc[j]) * sc[k];
+                    }
+                    out[e] = S;
+                }
             }
-            for (; t < t1; ++t) S += tp[t * E + e];
-            if (shift) {
-                const double sk = sm[k], ck = sm[p + k];
-                S = ((S + cj * sk) + ck * sj) + ncj * ck;
-            }
-            out[e] = S;
+            __syncthreads();
         }
     }
 }
@@ -211,7 +235,12 @@ cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_
                               const double* shift, uint32_t n_ranges, uint32_t p, uint64_t first_range,
                               double* rank_buf, uint32_t* flags, cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
-    k_range_fold<<<n_ranges, 256, 2 * p * sizeof(double), stream>>>(tile_partials, tile_prefix, range_count, shift, p,
+    const size_t smem = (2 * p + kFoldLanes * 32) * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_range_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k_range_fold<<<n_ranges, 256, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, p,
                                                                      first_range, rank_buf, flags);
     return cudaGetLastError();
 }

@@ -105,6 +105,17 @@ class Partition:
     def total_rows(self) -> int:
         return sum(r.row_count for r in self.ranges)
 
+    def arrays(self):
+        """(starts, counts) as uint64 arrays for the C ABI, cached while the ranges are unchanged."""
+        key = (id(self.ranges), len(self.ranges), self.ranges[-1] if self.ranges else None)
+        cached = getattr(self, "_arrays", None)
+        if cached is None or cached[0] != key:
+            starts = np.fromiter((r.start_row for r in self.ranges), dtype=np.uint64, count=len(self.ranges))
+            counts = np.fromiter((r.row_count for r in self.ranges), dtype=np.uint64, count=len(self.ranges))
+            cached = (key, starts, counts)
+            self._arrays = cached
+        return cached[1], cached[2]
+
 
 @dataclass
 class ReductionPlan:
@@ -369,8 +380,7 @@ class Engine:
             src.first_row = first_row
             src.n_rows = rows
         R = len(plan.partition.ranges)
-        starts = np.array([r.start_row for r in plan.partition.ranges], dtype=np.uint64)
-        counts = np.array([r.row_count for r in plan.partition.ranges], dtype=np.uint64)
+        starts, counts = plan.partition.arrays()
         out = SuffStats.empty(schema, plan.precision)
         n = ctypes.c_uint64()
         err = N.Error()
