@@ -43,7 +43,10 @@ CONFIGS = {
                                    "Gaussian, mu=1), HBM-resident"),
     "c1": (1_000_000, 9, 1, 0, "C1: 1e6 rows x (8 FP64 Gaussian + 1 ID) per GPU, HBM-resident"),
     "c3": (125_000_000, 16, 0, 2, "C3 shard: 1.25e8 rows x 16 per GPU (1e9 over 8 GPUs), HBM-resident"),
+    "c5": (50_000_000, 256, 2, 0, "C5 shard: 5e7 rows x 256 FP64 Gaussian cols per GPU (the 1e8 x 256 = 204.8 GB "
+                                  "config over 2 GPUs), HBM-resident, FP64 DMMA SYRK"),
 }
+DMMA_PEAK_TFLOPS = 37.03  # measured: profiles/r01_fp64_probe.log (mma.sync m8n8k4 f64, 148 SMs)
 CHUNK_ROWS = 1 << 20
 SEED, MU = 42, 1.0
 CPU_SAMPLE_ROWS = 20_000_000  # reference CPU arm: 2e7 rows x 16 (2.56 GB SSTATBIN in /dev/shm)
@@ -67,37 +70,48 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self._stop = threading.Event()
+        self.rows = []  # (host time, fields)
+        self.window = None
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                self.rows.append([x.strip() for x in out.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                           "--format=csv,noheader,nounits", "-lms", "20"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            for line in self._proc.stdout:
+                self.rows.append((time.perf_counter(), [x.strip() for x in line.strip().split(",")]))
+        except Exception:
+            pass
 
-    def __enter__(self):
+    def start(self):
         self._t.start()
-        return self
+        time.sleep(0.3)  # nvidia-smi needs a moment before its first line
 
-    def __exit__(self, *a):
-        self._stop.set()
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self._proc is not None:
+            self._proc.terminate()
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
+        if not self.rows or self.window is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        t0, t1 = self.window
+        inside = [r for t, r in self.rows if t0 <= t <= t1]
+        note = "samples inside the timed region"
+        if len(inside) < 3:  # short timed region: widen to the adjacent warm-up/drain samples
+            inside = [r for t, r in self.rows if t0 - 0.25 <= t <= t1 + 0.25]
+            note = "timed region +-0.25 s (region shorter than the 20 ms sampling period x 3)"
+        sm = [float(r[0]) for r in inside if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in inside if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in inside for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(inside), "note": note}
 
 
 def dist_env():
@@ -229,25 +243,29 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         step()
     kern, launches = [], 0
+    clocks = ClockSampler(local)
+    clocks.start()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        e0.record(stream)
-        for _ in range(args.steps):
-            res = step()
-            kern.append(eng.last_timings.kernel_seconds)
-            launches += eng.last_timings.kernel_launches
-        e1.record(stream)
-        torch.cuda.synchronize()
+    t_start = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+        kern.append(eng.last_timings.kernel_seconds)
+        launches += eng.last_timings.kernel_launches
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark(t_start, time.perf_counter())
     barrier()
+    clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     kern_s = max_over_ranks(sum(kern) / len(kern))
     value = n_global / (ms * 1e-3)
 
     # ---- e2e: public API from pinned host memory (H2D + result D2H every step) ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and p <= 64:
         H = D.cpu().pin_memory()
         del D
         torch.cuda.empty_cache()
@@ -269,7 +287,7 @@ def run_ours(args):
                "h2d_gb_per_s_per_gpu": local_rows * p * 8 / dt / 1e9}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and p == 16:
         rates, cores, split = cpu_reference_rows_per_s(steps=3, warmup=1)
         cpu = {"value": statistics.median(rates), "unit": "rows/s", "cores": cores, "kind": "reference",
                "sample": f"reference dataset_suffstats (oracle/_ref) over {CPU_SAMPLE_ROWS} rows x {p} of the same "
@@ -279,6 +297,18 @@ def run_ours(args):
         peak, peak_src = peaks()
         bytes_per_launch = local_rows * p * 8
         achieved = bytes_per_launch / kern_s / 1e9
+        if p > 64:  # compute-bound: FP64 tensor-pipe roofline, p(p+2) flops per row
+            flops = local_rows * p * (p + 2)
+            roof = {"bound": "tensor", "achieved": flops / kern_s / 1e12, "peak": DMMA_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": flops / kern_s / 1e12 / DMMA_PEAK_TFLOPS, "traffic": None,
+                    "kernel": "k_widep (K2)", "per_launch_flops": flops, "per_launch_ms": kern_s * 1e3,
+                    "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_probe.log; MEASURED_PEAKS.json "
+                                   "has no FP64 entry)", "hbm_gb_per_s": achieved}
+        else:
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": f"k_smallp<{(p + 7) // 8},{str(p % 16 == 0).lower()}> (K1)",
+                    "per_launch_bytes": bytes_per_launch, "per_launch_ms": kern_s * 1e3, "peak_source": peak_src}
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -286,14 +316,11 @@ def run_ours(args):
             "data": "synthetic (bit-portable SplitMix64 RowRng generator, same bytes as the CPU oracle)",
             "config": {"workload": desc, "rows_per_gpu": local_rows, "global_rows": n_global, "p": p,
                        "chunk_rows": CHUNK_ROWS, "ranges": R,
-                       "l2": "no flush: 12.8 GB/GPU inputs are >100x the 126 MB L2",
+                       "l2": f"no flush: {local_rows * p * 8 / 1e9:.1f} GB/GPU inputs are >>126 MB L2",
                        "parallelism": f"{world} GPU row shards" + (", NCCL all-gather of per-range partials"
                                                                    if world > 1 else "")},
             "gb_per_s": value * 8 * p / 1e9,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_smallp<2,true> (K1)", "per_launch_bytes": bytes_per_launch,
-                         "per_launch_ms": kern_s * 1e3, "peak_source": peak_src},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

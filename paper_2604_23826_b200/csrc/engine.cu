@@ -269,7 +269,7 @@ struct Plan {
     std::vector<uint64_t> tile_row, tile_rows;  // host view of local tiles (streaming)
 };
 
-uint64_t tiles_of(uint64_t count) { return (count + kTileRows - 1) / kTileRows; }
+uint64_t tile_rows_for(uint32_t p) { return p > 64 ? widep_tile_rows(p) : kTileRows; }
 
 struct Outcome {
     uint64_t bad_lin = kNone;  // lowest first-non-finite linear index over all ranks
@@ -427,6 +427,8 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     // ---- local plan → device ----
     CUDA_TRY(c->h_meta.reserve((3 * L + 1) * 8));
     uint64_t* hm = c->h_meta.as<uint64_t>();
+    const uint64_t TR = tile_rows_for(p);
+    auto tiles_of = [TR](uint64_t count) { return (count + TR - 1) / TR; };
     uint64_t nt = 0;
     for (uint64_t i = 0; i < L; ++i) {
         hm[i] = P.starts[P.r0 + i];
@@ -539,8 +541,8 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             for (uint64_t i = 0, t = 0; i < L; ++i) {
                 const uint64_t rs = P.starts[P.r0 + i], rc = P.counts[P.r0 + i];
                 for (uint64_t q = 0; q < tiles_of(rc); ++q, ++t) {
-                    trow[t] = rs + q * kTileRows;
-                    trows[t] = std::min<uint64_t>(kTileRows, rs + rc - trow[t]);
+                    trow[t] = rs + q * TR;
+                    trows[t] = std::min<uint64_t>(TR, rs + rc - trow[t]);
                 }
             }
             stream_chunks(c, hr, trow, trows,

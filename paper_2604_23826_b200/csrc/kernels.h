@@ -12,8 +12,9 @@ namespace sstat_b200 {
 // min(tiles, sms x resident CTAs per SM).
 cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream);
 
-// K2: tiles for p > 64 (smem-staged DMMA SYRK).
+// K2: tiles for p > 64 (smem-staged DMMA SYRK), tiles of widep_tile_rows(p) rows.
 cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream);
+uint32_t widep_tile_rows(uint32_t p);
 
 // shift[r][j] = first row of local range r (0 when the range is empty).
 cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uint64_t* range_start,

@@ -372,3 +372,61 @@ def test_c2_full_size_properties(engine):
     assert np.max(np.abs(g - want)) < 2e-3
     del D
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["wide_p80", "wide_p256"])
+def test_wide_p_cases(engine, oracle, reference, golden, name):
+    """K2 (p > 64, DMMA SYRK) against the reference: sums bit-pinned golden, X^T X via the
+    oracle (pinned to the reference by SHA-256), eigenvalues via the reference's run_pca."""
+    torch = torch_mod()
+    c = golden[name]
+    g = c["gen"]
+    p = g["p"]
+    X = oracle.generate(g["kind"], g["seed"], g["mu"], g["n_int"], 0, g["n"], p)
+    assert sha(X) == c["input_sha256"]
+    s0, c0 = oracle.plan_partitions(g["n"], g["chunk"])
+    wn, ws, wS = oracle.run_reduction(X, p, s0, c0, 8)
+    assert sha(wS) == c["cross_sha256"], "oracle X^T X no longer matches the reference"
+    D = to_dev(X)
+    for flags in (0, 1):
+        got = engine.dataset_suffstats(D, schema(p), plan(g["n"], g["chunk"]), flags=flags)
+        check_against(got, wn, unhex(c["sums"]), wS)
+    exact = engine.dataset_suffstats(D, schema(p), plan(g["n"], g["chunk"]), flags=2)
+    assert np.array_equal(bits(exact.cross), bits(wS)) and np.array_equal(bits(exact.sums), bits(unhex(c["sums"])))
+    got = engine.dataset_suffstats(D, schema(p), plan(g["n"], g["chunk"]))
+    for basis, key in ((1, "pca_corr_eigenvalues"), (0, "pca_cov_eigenvalues")):
+        ev = reference.run_pca(p, [], got.n, got.sums, got.cross, basis=basis)
+        rev = unhex(c[key])
+        assert np.max(np.abs(ev - rev) / np.abs(rev)) <= 1e-10
+    # host-streamed source gives the same bits
+    assert engine.dataset_suffstats(X, schema(p), plan(g["n"], g["chunk"])).bit_equal(got)
+
+
+@pytest.mark.parametrize("p", [65, 72, 97, 128, 130, 200])
+def test_wide_p_shapes_vs_truth(engine, oracle, p):
+    """Odd / ragged wide p (masked column blocks, 8-byte staging for odd p), ragged ranges."""
+    rng = np.random.default_rng(p)
+    n = 70001
+    X = rng.normal(1.0, 1.0, size=(n, p))
+    X[:, 0] = rng.integers(1, 100, size=n)
+    X[:, 1] = rng.integers(1, 100, size=n)
+    ts, tS = truth_suffstats(X)
+    got = engine.dataset_suffstats(to_dev(X), schema(p), plan(n, 33333))
+    check_against(got, n, ts, tS)
+    assert np.array_equal(bits(got.cross[[0, 1, p]]), bits(tS[[0, 1, p]]))  # integer block exact
+
+
+def test_c5_scale_wide(engine):
+    """Config 5 shape (p = 256) at 4e6 rows on one GPU (the full 1e8 x 256 = 204.8 GB needs
+    two B200s): fast vs reference-order mode."""
+    torch = torch_mod()
+    n, p = 4_000_000, 256
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 2, 19, 1.0, 0, 0, n, p)
+    pl = plan(n, 1 << 20)
+    fast = engine.dataset_suffstats(D, schema(p), pl)
+    exact = engine.dataset_suffstats(D, schema(p), pl, flags=2)
+    assert cs_err(fast.cross, exact.cross, p) <= TOL
+    assert sums_err(fast.sums, exact.sums, exact.cross, n, p) <= TOL
+    del D
+    torch.cuda.empty_cache()
