@@ -46,6 +46,54 @@ __global__ void dmma_peak(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// 4x4 outer product of 8 distinct operand registers (the K2 inner loop without loads)
+__global__ void dmma_outer(double* out, int iters) {
+  double acc[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+  double f[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) f[a] = threadIdx.x * 1e-3 + a;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma(acc[a * 4 + b][0], acc[a * 4 + b][1], f[a], f[4 + b]);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i][0] + acc[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// same, with the operands re-read from shared memory and shifted every k-step (K2's loop)
+__global__ void dmma_outer_lds(double* out, int iters) {
+  __shared__ double st[4 * 264];
+  for (int i = threadIdx.x; i < 4 * 264; i += blockDim.x) st[i] = i * 1e-3;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, kk = lane & 3;
+  double acc[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+  double c[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) c[a] = a * 0.5;
+  const double* rowp = st + kk * 260 + g;
+  for (int i = 0; i < iters; ++i) {
+    double f[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) f[a] = rowp[8 * a + (i & 1) * 64] - c[a];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma(acc[a * 4 + b][0], acc[a * 4 + b][1], f[a], f[4 + b]);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i][0] + acc[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void stream_read(const double2* __restrict__ x, size_t n2, double* out) {
   double s0 = 0, s1 = 0;
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -162,6 +210,22 @@ int main() {
     std::printf("DMMA nacc=%d wpb=%d: %.2f TFLOP/s (%.1f FMA/clk/SM at base clk)\n", nacc, warps_per_block, 2 * fma / ms / 1e9,
                 fma / (ms * 1e-3) / sms / (clk * 1e3));
   };
+  // occupancy sweep: warps per SM = blocks_per_sm * wpb (grid = sms * blocks_per_sm)
+  auto run_occ = [&](auto kern, int nacc, int wpb, int bpsm) {
+    int iters = 2048, blocks = sms * bpsm, threads = 32 * wpb;
+    kern<<<blocks, threads>>>(out, 16);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    kern<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    double fma = (double)blocks * wpb * iters * nacc * 256;
+    std::printf("DMMA occupancy: %2d warps/SM, %2d chains/warp: %.2f TFLOP/s\n", wpb * bpsm, nacc, 2 * fma / ms / 1e9);
+  };
+  for (int w : {1, 2, 4, 8}) run_occ(dmma_peak<16>, 16, w, 1);
+  for (int w : {4, 8, 16}) run_occ(dmma_outer, 16, w, 1);
+  for (int w : {4, 8, 16}) run_occ(dmma_outer_lds, 16, w, 1);
+  run_occ(dmma_peak<16>, 16, 4, 2);
+  run_occ(dmma_peak<16>, 16, 4, 4);
   run_dmma(dmma_peak<1>, 1, 4);
   run_dmma(dmma_peak<4>, 4, 4);
   run_dmma(dmma_peak<8>, 8, 8);
