@@ -172,12 +172,14 @@ int sstat_cuda_range_partials(sstat_cuda_ctx* ctx, const sstat_cuda_source* src,
 
 /* ---- host helpers (no device work) ---- */
 
-/* The ascending range fold over gathered per-rank buffers (host memory), the same code
- * the device runs after the all-gather: rank q's buffer starts at buf + q*rank_stride
- * with a 4-double header, then its ranges [floor(qR/W), floor((q+1)R/W)) of
- * p + p(p+1)/2 doubles each.  out receives p + p(p+1)/2 doubles. */
+/* The range fold over gathered per-rank buffers (host memory), the same code the device
+ * runs after the all-gather: rank q's buffer starts at buf + q*rank_stride with a
+ * 4-double header, then its ranges [floor(qR/W), floor((q+1)R/W)) of p + p(p+1)/2
+ * doubles each.  flags & SSTAT_FLAG_REFEXACT (or Binary32Diagnostic): the reference's
+ * ascending fold from +0.0; otherwise the 8-lane fast fold of the default mode.
+ * out receives p + p(p+1)/2 doubles. */
 int sstat_fold_ranges_host(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
-                           uint32_t precision, double* out);
+                           uint32_t precision, uint32_t flags, double* out);
 
 /* plan_partitions: returns the range count (0 on invalid input, like the reference's
  * invalid_argument); fills starts/counts when non-NULL. */

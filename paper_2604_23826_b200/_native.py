@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, Structure, c_char, c_char_p, c_double, c_int, c_size_t, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsstat_b200.so")
+LIB_PATH = os.environ.get("SSTAT_LIB", os.path.join(HERE, "libsstat_b200.so"))
 
 # sstat_status
 OK = 0
@@ -139,7 +139,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             [c_void_p, P(Source), c_uint32, c_void_p, c_void_p, c_uint64, c_uint64, c_uint64, c_uint32, c_uint32, dp,
              P(Error)],
         ),
-        "sstat_fold_ranges_host": (c_int, [dp, c_uint64, c_uint64, c_int, c_uint32, c_uint32, dp]),
+        "sstat_fold_ranges_host": (c_int, [dp, c_uint64, c_uint64, c_int, c_uint32, c_uint32, c_uint32, dp]),
         "sstat_plan_partitions": (c_uint64, [c_uint64, c_uint64, c_void_p, c_void_p]),
         "sstat_merge": (c_int, [c_uint32, c_uint32, u64p, dp, dp, c_uint64, dp, dp]),
         "sstat_cuda_generate": (

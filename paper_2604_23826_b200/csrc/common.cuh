@@ -30,7 +30,8 @@ struct TileJob {
     const uint64_t* range_start;   // [n_ranges] absolute first row of each local range
     const uint64_t* range_count;   // [n_ranges]
     const uint64_t* tile_prefix;   // [n_ranges + 1] local range r owns tiles [prefix[r], prefix[r+1])
-    const double* shift;           // [n_ranges][p] first row of each range, or nullptr
+    const double* shift;           // [n_ranges][p] first row of each range, or nullptr (see below)
+    uint32_t shift_from_base;      // shift == nullptr: 1 = c is the range's first row read from base
     uint32_t n_ranges;
     uint32_t p;
     uint64_t tile_begin, tile_end; // tiles of this launch
@@ -65,12 +66,43 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) { return __ldcs(r
 // (UINT64_MAX = none), [1] first non-finite linear index row*p + col.
 constexpr uint32_t kHdr = 4;
 
+// Where range r's partial sits in the gathered rank buffers: rank q = owner(r) with
+// first(q) = floor(q R / W), at buf + q*rank_stride + kHdr + (r - first(q))*E.
+__host__ __device__ inline const double* range_partial(const double* buf, uint64_t rank_stride, uint64_t n_ranges,
+                                                       int world, uint64_t E, uint64_t r) {
+    if (world == 1) return buf + kHdr + r * E;
+    int q = (int)((r * (uint64_t)world) / n_ranges);
+    if (q >= world) q = world - 1;
+    while (q > 0 && (uint64_t)q * n_ranges / world > r) --q;
+    while (q + 1 < world && (uint64_t)(q + 1) * n_ranges / world <= r) ++q;
+    return buf + (uint64_t)q * rank_stride + kHdr + (r - (uint64_t)q * n_ranges / world) * E;
+}
+
+// Fast-mode range fold of one entry: 8 interleaved lanes (lane q sums ranges q, q+8, ...
+// ascending from +0.0), then the lanes in order 0..7.  A fixed function of the global range
+// sequence — identical on every rank and for any GPU count — with 8x shorter dependent
+// chains than the reference order.  fold_lane is one lane (device: one thread per lane).
+constexpr int kFoldLanes = 8;
+__host__ __device__ inline double fold_lane(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world,
+                                            uint64_t E, uint64_t e, int q) {
+    double s = 0.0;
+    for (uint64_t r = q; r < n_ranges; r += kFoldLanes) s += range_partial(buf, rank_stride, n_ranges, world, E, r)[e];
+    return s;
+}
+__host__ __device__ inline double fold_fast(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world,
+                                            uint64_t E, uint64_t e) {
+    double t = 0.0;
+    for (int q = 0; q < kFoldLanes; ++q) t += fold_lane(buf, rank_stride, n_ranges, world, E, e, q);
+    return t;
+}
+
 // The ascending range fold of one entry (reference include/sstat/reduce.hpp:142-145 with
 // merge_suffstats, src/suffstats.cpp:86-105): acc starts at +0.0 and adds range 0, 1, ...
 // Range r sits in rank q = owner(r), first(q) = floor(q R / W), at
 //   buf + q*rank_stride + kHdr + (r - first(q))*E + e.
-// Binary32 mode rounds every add through float like merge_suffstats.  Shared by the
-// device fold (K3b) and the host fold used to check the rank layout.
+// Binary32 mode rounds every add through float like merge_suffstats.  The reference-order
+// fold of SSTAT_FLAG_REFEXACT / Binary32Diagnostic; shared by the device fold (K3b) and the
+// host fold used to check the rank layout.
 __host__ __device__ inline double fold_entry(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world,
                                              uint32_t p, uint32_t precision, uint64_t e) {
     const uint64_t E = partial_len(p);

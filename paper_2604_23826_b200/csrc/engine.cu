@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -457,15 +458,20 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     }
     const double* d_shift = shift ? c->d_shift.as<double>() : nullptr;
     const bool wide = p > 64;
+    // Folding ranges inside K1 (last CTA of a range folds it) was measured and rejected: the
+    // folds' L2/HBM round trips under the streaming load stretch K1's tail by ~0.5 ms, far
+    // more than the ~40 us the separate K3a/K3b launches cost.
+    CUDA_TRY(c->d_result.reserve(E * 8));
 
-    auto tile_job = [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
-        TileJob j;
+    auto tile_job = [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1, bool shift_in_base) {
+        TileJob j{};
         j.base = base;
         j.base_row = base_row;
         j.range_start = d_starts;
         j.range_count = d_counts;
         j.tile_prefix = d_prefix;
-        j.shift = d_shift;
+        j.shift = shift_in_base ? nullptr : d_shift;
+        j.shift_from_base = shift_in_base ? 1u : 0u;
         j.n_ranges = (uint32_t)L;
         j.p = p;
         j.tile_begin = t0;
@@ -476,6 +482,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
 
     CUDA_TRY(cudaEventRecord(c->ev[0], s));
     if (tm) tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
+    bool scanned = false;  // the non-finite scan already ran for this rank
     if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
         const double* base = static_cast<const double*>(src->ptr);
         const uint64_t base_row = src->first_row;
@@ -485,18 +492,29 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
             if (tm) tm->kernel_launches += 1;
         } else {
-            if (shift) CUDA_TRY(launch_gather_shift(base, base_row, d_starts, d_counts, (uint32_t)L, p, c->d_shift.as<double>(), s));
+            // K1 and K3a read the shift rows in place from the resident shard; K2 takes a table
+            if (shift && wide) {
+                CUDA_TRY(launch_gather_shift(base, base_row, d_starts, d_counts, (uint32_t)L, p, c->d_shift.as<double>(), s));
+                if (tm) tm->kernel_launches += 1;
+            }
+            const bool in_place = shift && !wide;
             CUDA_TRY(cudaEventRecord(c->ev[0], s));  // kernel_seconds brackets K1/K2 alone
-            if (nt > 0) tile_job(base, base_row, 0, nt);
+            if (nt > 0) tile_job(base, base_row, 0, nt, in_place);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
-            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, (uint32_t)L, p, P.r0,
-                                       rank_buf, d_flags, s));
-            if (tm) tm->kernel_launches += 2 + (shift ? 1 : 0);
+            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, in_place ? nullptr : d_shift,
+                                       in_place ? base : nullptr, base_row, d_starts, (uint32_t)L, p, P.r0, rank_buf,
+                                       d_flags, s));
+            if (tm) tm->kernel_launches += 2;
         }
-        CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_counts, (uint32_t)L, p, d_flags, rank_buf,
-                                       c->sms * 2, s));
+        if (world > 1 || P.mode == Mode::Partials) {
+            // every rank must know its first non-finite before the exchange; on one GPU the
+            // scan runs only when a range was flagged (after the result read-back)
+            CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_counts, (uint32_t)L, p, d_flags, rank_buf,
+                                           c->sms * 2, s));
+            if (tm) tm->kernel_launches += 1;
+            scanned = true;
+        }
         CUDA_TRY(cudaEventRecord(c->ev[2], s));
-        if (tm) tm->kernel_launches += 1;
     } else if (L > 0) {
         // ---- host / file source: pinned staging ring, copy stream || compute stream ----
         cudaPointerAttributes attr{};
@@ -547,12 +565,13 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             }
             stream_chunks(c, hr, trow, trows,
                           [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
-                              tile_job(base, base_row, t0, t1);
+                              tile_job(base, base_row, t0, t1, false);
                           },
                           tm);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
-            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, (uint32_t)L, p, P.r0,
-                                       rank_buf, d_flags, s));
+            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
+                                       (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
+            if (tm) tm->kernel_launches += 1;
         }
         // Non-finite localisation: re-stream only the flagged ranges (error path).
         CUDA_TRY(c->h_flags.reserve(L * 4));
@@ -592,6 +611,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                               nullptr);
             }
         }
+        scanned = true;
         CUDA_TRY(cudaEventRecord(c->ev[2], s));
     } else {
         CUDA_TRY(cudaEventRecord(c->ev[1], s));
@@ -617,10 +637,10 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         fold_buf = c->d_gather.as<double>();
     }
     CUDA_TRY(cudaEventRecord(c->ev[3], s));
-    CUDA_TRY(c->d_result.reserve(E * 8));
-    CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, c->d_result.as<double>(), s));
-    CUDA_TRY(cudaEventRecord(c->ev[4], s));
+    CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, refexact,
+                               c->d_result.as<double>(), s));
     if (tm) tm->kernel_launches += 1;
+    CUDA_TRY(cudaEventRecord(c->ev[4], s));
     CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
     double* hres = c->h_result.as<double>();
     CUDA_TRY(cudaMemcpyAsync(hres, c->d_result.p, E * 8, cudaMemcpyDeviceToHost, s));
@@ -628,6 +648,16 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         CUDA_TRY(cudaMemcpyAsync(hres + E + q * kHdr, fold_buf + q * rank_stride, kHdr * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
+    if (!scanned && world == 1 && L > 0) {
+        uint64_t flagged;
+        std::memcpy(&flagged, hres + E, 8);
+        if (flagged != kNone) {  // error path: locate the first non-finite value of the flagged ranges
+            CUDA_TRY(launch_find_nonfinite(static_cast<const double*>(src->ptr), src->first_row, d_starts, d_counts,
+                                           (uint32_t)L, p, d_flags, rank_buf, c->sms * 2, s));
+            CUDA_TRY(cudaMemcpyAsync(hres + E, rank_buf, kHdr * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+    }
     for (int q = 0; q < world; ++q) {
         uint64_t lin;
         std::memcpy(&lin, hres + E + q * kHdr + 1, 8);
@@ -946,10 +976,13 @@ int sstat_cuda_range_partials(sstat_cuda_ctx* c, const sstat_cuda_source* src, u
 }
 
 int sstat_fold_ranges_host(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
-                           uint32_t precision, double* out) {
+                           uint32_t precision, uint32_t flags, double* out) {
     if (!buf || !out || world < 1 || p == 0 || precision > 1) return SSTAT_ERR_INVALID;
     const uint64_t E = partial_len(p);
-    for (uint64_t e = 0; e < E; ++e) out[e] = fold_entry(buf, rank_stride, n_ranges, world, p, precision, e);
+    const bool reference_order = (flags & SSTAT_FLAG_REFEXACT) || precision == 1;
+    for (uint64_t e = 0; e < E; ++e)
+        out[e] = reference_order ? fold_entry(buf, rank_stride, n_ranges, world, p, precision, e)
+                                 : fold_fast(buf, rank_stride, n_ranges, world, E, e);
     return SSTAT_OK;
 }
 

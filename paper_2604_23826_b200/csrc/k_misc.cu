@@ -3,6 +3,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "fold.cuh"
 #include "kernels.h"
 
 namespace sstat_b200 {
@@ -12,19 +13,6 @@ using ull = unsigned long long;
 
 __device__ __forceinline__ bool finite64(double v) { return isfinite(v); }
 
-// Inverse of packed_index: (j, k) with j <= k for packed position i.
-__device__ __forceinline__ void unpack_index(uint32_t p, uint32_t i, uint32_t& j, uint32_t& k) {
-    // row j: start(j) = j*p - j(j-1)/2 <= i < start(j+1); estimate then correct
-    const double b = 2.0 * p + 1.0;
-    int64_t row = (int64_t)floor((b - sqrt(b * b - 8.0 * i)) * 0.5);
-    if (row < 0) row = 0;
-    auto start = [p](int64_t jj) { return jj * (int64_t)p - jj * (jj - 1) / 2; };
-    while (row > 0 && start(row) > (int64_t)i) --row;
-    while (row + 1 < (int64_t)p && start(row + 1) <= (int64_t)i) ++row;
-    j = (uint32_t)row;
-    k = (uint32_t)(row + ((int64_t)i - start(row)));
-}
-
 __global__ void k_gather_shift(const double* __restrict__ base, uint64_t base_row, const uint64_t* __restrict__ range_start,
                                const uint64_t* __restrict__ range_count, uint32_t n_ranges, uint32_t p, double* shift) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -33,76 +21,23 @@ __global__ void k_gather_shift(const double* __restrict__ base, uint64_t base_ro
     shift[i] = range_count[r] ? base[(range_start[r] - base_row) * p + j] : 0.0;
 }
 
-// Lane q of kFoldLanes sums tiles t0+q, t0+q+kFoldLanes, ... of entry e (8 loads in flight).
-constexpr int kFoldLanes = 8;
-
-__device__ __forceinline__ double fold_tiles_lane(const double* __restrict__ tp, uint64_t E, uint64_t e, uint64_t t0,
-                                                  uint64_t t1, int q) {
-    double s = 0.0;
-    uint64_t t = t0 + q;
-    for (; t + 7 * kFoldLanes < t1; t += 8 * kFoldLanes) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = tp[(t + u * kFoldLanes) * E + e];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
-    }
-    for (; t < t1; t += kFoldLanes) s += tp[t * E + e];
-    return s;
-}
-
-// One block (8 warps) per local range.  Tile partials of the range are summed in a fixed
-// order (8 interleaved lanes, then lane 0..7), and the shifted moments are mapped back to
-// raw moments with c = shift row, n = range rows:
-//   s_j  = s'_j + n c_j
-//   S_jk = S'_jk + c_j s'_k + c_k s'_j + n c_j c_k
-// (exact for integer data below 2^53, like the reference's own sums).
+// K3a: one block (256 threads) per local range (fold_range_block, shared with K1's fused path).
+// The shift row comes from the table, or (shift == nullptr, base != nullptr) in place as the
+// range's first row of the resident shard.
 __global__ void __launch_bounds__(256) k_range_fold(const double* __restrict__ tp,
                                                     const uint64_t* __restrict__ tile_prefix,
                                                     const uint64_t* __restrict__ range_count,
-                                                    const double* __restrict__ shift, uint32_t p,
-                                                    uint64_t first_range, double* rank_buf, uint32_t* flags) {
-    extern __shared__ double sm[];  // [p] shifted sums, [p] shift, [kFoldLanes][32] lane partials
-    double* ssum = sm;
-    double* sc = sm + p;
-    double* lanes = sm + 2 * p;
+                                                    const double* __restrict__ shift, const double* base,
+                                                    uint64_t base_row, const uint64_t* __restrict__ range_start,
+                                                    uint32_t p, uint64_t first_range, double* rank_buf,
+                                                    uint32_t* flags, uint64_t slice) {
+    extern __shared__ double sm[];
     const uint32_t r = blockIdx.x;
-    const uint64_t E = partial_len(p);
-    const uint64_t t0 = tile_prefix[r], t1 = tile_prefix[r + 1];
-    const double n = (double)range_count[r];
-    double* out = rank_buf + kHdr + (uint64_t)r * E;
-    const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
-    for (int phase = 0; phase < 2; ++phase) {
-        const uint64_t lo = phase == 0 ? 0 : p, hi = phase == 0 ? p : E;
-        for (uint64_t e0 = lo; e0 < hi; e0 += 32) {
-            const uint64_t e = e0 + le;
-            lanes[q * 32 + le] = e < hi ? fold_tiles_lane(tp, E, e, t0, t1, q) : 0.0;
-            __syncthreads();
-            if (q == 0 && e < hi) {
-                double S = lanes[le];
-#pragma unroll
-                for (int w = 1; w < kFoldLanes; ++w) S += lanes[w * 32 + le];
-                if (phase == 0) {
-                    const double cj = shift ? shift[(uint64_t)r * p + e] : 0.0;
-                    ssum[e] = S;
-                    sc[e] = cj;
-                    out[e] = S + n * cj;
-                    if (!finite64(S) || !finite64(cj)) {
-                        flags[r] = 1;
-                        atomicMin(reinterpret_cast<ull*>(rank_buf), (ull)(first_range + r));
-                    }
-                } else {
-                    if (shift) {
-                        uint32_t j, k;
-                        unpack_index(p, (uint32_t)(e - p), j, k);
-                        S = ((S + sc[j] * ssum[k]) + sc[k] * ssum[j]) + (n * sc[j]) * sc[k];
-                    }
-                    out[e] = S;
-                }
-            }
-            __syncthreads();
-        }
-    }
+    const double* c = shift ? shift + (uint64_t)r * p
+                            : (base && range_count[r] ? base + (range_start[r] - base_row) * p : nullptr);
+    const uint64_t x0 = (uint64_t)blockIdx.y * slice, x1 = x0 + slice;  // this block's cross entries
+    fold_range_block(tp, tile_prefix[r], tile_prefix[r + 1], (double)range_count[r], c, p, first_range + r,
+                     rank_buf + kHdr + (uint64_t)r * partial_len(p), rank_buf, flags + r, sm, x0, x1);
 }
 
 // Scans the flagged local ranges for their first non-finite value.  Ranges ascend, so
@@ -121,11 +56,32 @@ __global__ void k_find_nonfinite(const double* __restrict__ base, uint64_t base_
     }
 }
 
-__global__ void k_final_fold(const double* __restrict__ buf, uint64_t rank_stride, uint64_t n_ranges, int world,
-                             uint32_t p, uint32_t precision, double* out) {
+// K3b, reference order (SSTAT_FLAG_REFEXACT / Binary32Diagnostic): one thread per entry.
+__global__ void k_final_fold_seq(const double* __restrict__ buf, uint64_t rank_stride, uint64_t n_ranges, int world,
+                                 uint32_t p, uint32_t precision, double* out) {
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (e >= partial_len(p)) return;
     out[e] = fold_entry(buf, rank_stride, n_ranges, world, p, precision, e);
+}
+
+// K3b, fast mode (fold_fast): blocks of 256 threads over 32-entry slices.
+__global__ void __launch_bounds__(256) k_final_fold_fast(const double* __restrict__ buf, uint64_t rank_stride,
+                                                         uint64_t n_ranges, int world, uint32_t p, double* out) {
+    __shared__ double sm[256];
+    const uint64_t E = partial_len(p);
+    const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const uint64_t e = blockIdx.x * 32ull + le;
+    double s = 0.0;
+    if (e < E)
+        for (uint64_t r = q; r < n_ranges; r += kFoldLanes) s += range_partial(buf, rank_stride, n_ranges, world, E, r)[e];
+    sm[q * 32 + le] = s;
+    __syncthreads();
+    if (q == 0 && e < E) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kFoldLanes; ++w) t += sm[w * 32 + le];
+        out[e] = t;
+    }
 }
 
 template <typename Acc>
@@ -232,16 +188,22 @@ cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uin
 }
 
 cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_prefix, const uint64_t* range_count,
-                              const double* shift, uint32_t n_ranges, uint32_t p, uint64_t first_range,
-                              double* rank_buf, uint32_t* flags, cudaStream_t stream) {
+                              const double* shift, const double* base, uint64_t base_row, const uint64_t* range_start,
+                              uint32_t n_ranges, uint32_t p, uint64_t first_range, double* rank_buf, uint32_t* flags,
+                              cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
-    const size_t smem = (2 * p + kFoldLanes * 32) * sizeof(double);
+    const size_t smem = (2 * p + kFoldLanes * 32) * sizeof(double);  // fold_range_block scratch
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_range_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_range_fold<<<n_ranges, 256, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, p,
-                                                                     first_range, rank_buf, flags);
+    // blocks = ranges x slices of the cross entries; a slice is as wide as the sums so the
+    // redundant sums fold costs at most as much as the slice itself
+    const uint64_t cross = (uint64_t)p * (p + 1) / 2;
+    const uint64_t slice = 32ull * ((p + 31) / 32);
+    const dim3 grid(n_ranges, (unsigned)((cross + slice - 1) / slice));
+    k_range_fold<<<grid, 256, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, base, base_row,
+                                              range_start, p, first_range, rank_buf, flags, slice);
     return cudaGetLastError();
 }
 
@@ -254,9 +216,13 @@ cudaError_t launch_find_nonfinite(const double* base, uint64_t base_row, const u
 }
 
 cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
-                              uint32_t precision, double* out, cudaStream_t stream) {
+                              uint32_t precision, bool reference_order, double* out, cudaStream_t stream) {
     const uint64_t E = partial_len(p);
-    k_final_fold<<<(unsigned)((E + 127) / 128), 128, 0, stream>>>(buf, rank_stride, n_ranges, world, p, precision, out);
+    if (reference_order)
+        k_final_fold_seq<<<(unsigned)((E + 127) / 128), 128, 0, stream>>>(buf, rank_stride, n_ranges, world, p, precision,
+                                                                           out);
+    else
+        k_final_fold_fast<<<(unsigned)((E + 31) / 32), 256, 0, stream>>>(buf, rank_stride, n_ranges, world, p, out);
     return cudaGetLastError();
 }
 

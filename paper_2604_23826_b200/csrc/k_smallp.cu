@@ -16,6 +16,8 @@
 // Column permutation col(J, g):  VEC (p == 8*NB, NB even): g*NB + J  — each lane reads
 // NB contiguous doubles with 128-bit loads;  otherwise J*8 + g — 8 lanes read 8
 // consecutive doubles of a row per instruction (64-byte segments).
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,7 +27,10 @@ namespace {
 template <int NB, bool VEC>
 struct SmallP {
     static constexpr int NBLK = NB * (NB + 1) / 2;
-    static constexpr int U = NB <= 2 ? (VEC || NB == 1 ? 16 : 8) : (NB <= 4 ? 8 : 4);  // k-steps in flight per warp
+#ifndef SSTAT_U2V
+#define SSTAT_U2V 16
+#endif
+    static constexpr int U = NB <= 2 ? (VEC || NB == 1 ? SSTAT_U2V : 8) : (NB <= 4 ? 8 : 4);  // k-steps in flight per warp
     static constexpr int FRAG = NBLK * 64 + NB * 8;                // per-warp epilogue values
     __device__ __forceinline__ static int col(int J, int g) { return VEC ? g * NB + J : J * 8 + g; }
 };
@@ -91,8 +96,12 @@ __device__ int canonical_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
+// Memory-bound widths keep 4 CTAs (32 warps) per SM (64 registers at NB <= 2).
+template <int NB>
+constexpr int min_blocks() { return NB <= 2 ? 4 : (NB <= 4 ? 3 : 1); }
+
 template <int NB, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
+__global__ void __launch_bounds__(kThreads, min_blocks<NB>()) k_smallp(TileJob job) {
     using C = SmallP<NB, VEC>;
     constexpr int U = C::U;
     extern __shared__ double red[];  // [kWarps][FRAG]
@@ -109,11 +118,14 @@ __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
         const uint32_t rows = left < kTileRows ? (uint32_t)left : kTileRows;
         const double* __restrict__ tile = job.base + (row0 - job.base_row) * p;
 
+        // shift row c of this range: the precomputed table, or the range's first row in place
+        const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p
+                             : (job.shift_from_base ? job.base + (rs - job.base_row) * p : nullptr);
         double c[NB];
 #pragma unroll
         for (int J = 0; J < NB; ++J) {
             const int cj = C::col(J, g);
-            c[J] = (job.shift != nullptr && cj < (int)p) ? job.shift[(uint64_t)r * p + cj] : 0.0;
+            c[J] = (crow != nullptr && cj < (int)p) ? crow[cj] : 0.0;
         }
         double acc[C::NBLK][2];
         double s[NB];
@@ -183,11 +195,19 @@ __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
 template <int NB, bool VEC>
 cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, VEC>::FRAG;
-    cudaError_t e = cudaFuncSetAttribute(k_smallp<NB, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp<NB, VEC>, kThreads, smem);
-    if (e != cudaSuccess) return e;
+    // function attribute + occupancy, once per device (kept off the per-call path)
+    static std::atomic<int> cached[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = dev < 64 ? cached[dev].load() : 0;
+    if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_smallp<NB, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp<NB, VEC>, kThreads, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) per_sm = 1;
+        if (dev < 64) cached[dev].store(per_sm);
+    }
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;

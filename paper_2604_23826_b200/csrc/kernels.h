@@ -24,9 +24,12 @@ cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uin
 // K3a: fold each local range's tile partials in ascending tile order, map the shifted
 // moments back to raw sums / X^T X, write [kHdr + r*E] of `rank_buf`, and flag
 // non-finite ranges (global index first_range + r) in the header.
+// The shift row: shift[r*p], or (shift == nullptr, base != nullptr) the range's first row
+// read in place from the resident shard base (absolute row base_row at base[0]).
 cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_prefix, const uint64_t* range_count,
-                              const double* shift, uint32_t n_ranges, uint32_t p, uint64_t first_range,
-                              double* rank_buf, uint32_t* flags, cudaStream_t stream);
+                              const double* shift, const double* base, uint64_t base_row, const uint64_t* range_start,
+                              uint32_t n_ranges, uint32_t p, uint64_t first_range, double* rank_buf, uint32_t* flags,
+                              cudaStream_t stream);
 
 // First non-finite value (row-major) over the flagged local ranges (flags[r] != 0);
 // min absolute linear index row*p + col lands in header[1].  No-op when none flagged.
@@ -34,11 +37,12 @@ cudaError_t launch_find_nonfinite(const double* base, uint64_t base_row, const u
                                   const uint64_t* range_count, uint32_t n_ranges, uint32_t p, const uint32_t* flags,
                                   double* rank_buf, int grid, cudaStream_t stream);
 
-// K3b: ascending fold over all n_ranges global ranges from +0.0 (reduce.hpp:142-145).
+// K3b: fold over all n_ranges global ranges.  reference_order: ascending from +0.0
+// (reduce.hpp:142-145, fold_entry; precision 1 rounds every add through binary32 like
+// merge_suffstats, suffstats.cpp:92-98); otherwise the 8-lane fast fold (fold_fast).
 // Range r lives in rank q = owner(r) at buf + q*rank_stride + kHdr + (r - first(q))*E.
-// precision 1 rounds every add through binary32 (merge_suffstats, suffstats.cpp:92-98).
 cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
-                              uint32_t precision, double* out, cudaStream_t stream);
+                              uint32_t precision, bool reference_order, double* out, cudaStream_t stream);
 
 // Reference-order accumulation: one sequential mul-then-add chain per (range, entry)
 // exactly as accumulate_into<Acc> (suffstats.cpp:56-67); precision 1 = binary32.

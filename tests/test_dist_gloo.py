@@ -75,7 +75,7 @@ def _worker(rank, world, port, case, q):
         out = np.zeros(E)
         lib = N.load()
         dp = ctypes.POINTER(ctypes.c_double)
-        assert lib.sstat_fold_ranges_host(buf.ctypes.data_as(dp), stride, R, world, p, 0, out.ctypes.data_as(dp)) == 0
+        assert lib.sstat_fold_ranges_host(buf.ctypes.data_as(dp), stride, R, world, p, 0, 2, out.ctypes.data_as(dp)) == 0
         q.put((rank, "ok", out))
     finally:
         dist.destroy_process_group()

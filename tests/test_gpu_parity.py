@@ -286,7 +286,7 @@ def test_sharded_partials_fold_bit_identical(engine, oracle, W):
         buf[q * stride + 4: q * stride + 4 + out.size] = out
     res = np.zeros(E)
     dp = ctypes.POINTER(ctypes.c_double)
-    assert lib.sstat_fold_ranges_host(buf.ctypes.data_as(dp), stride, R, W, p, 0, res.ctypes.data_as(dp)) == 0
+    assert lib.sstat_fold_ranges_host(buf.ctypes.data_as(dp), stride, R, W, p, 0, 0, res.ctypes.data_as(dp)) == 0
     assert np.array_equal(bits(res[:p]), bits(whole.sums))
     assert np.array_equal(bits(res[p:]), bits(whole.cross))
 
