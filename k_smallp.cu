@@ -96,10 +96,13 @@ __device__ int canonical_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-// No occupancy floor: unbounded, NB <= 2 compiles to 64 registers (4 CTAs, 32 warps per SM)
-// and NB <= 4 to ~85 (3 CTAs); a cap only forces spills.
+// Occupancy floor: NB <= 4 keeps 3 CTAs per SM; NB <= 2 compiles to 64 registers by itself
+// (4 CTAs, 32 warps per SM) and a cap would only force spills.
+template <int NB>
+constexpr int min_blocks() { return NB <= 2 ? 1 : (NB <= 4 ? 3 : 1); }
+
 template <int NB, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
+__global__ void __launch_bounds__(kThreads, min_blocks<NB>()) k_smallp(TileJob job) {
     using C = SmallP<NB, VEC>;
     constexpr int U = C::U;
     extern __shared__ double red[];  // [kWarps][FRAG]
@@ -116,9 +119,9 @@ __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
         const uint32_t rows = left < kTileRows ? (uint32_t)left : kTileRows;
         const double* __restrict__ tile = job.base + (row0 - job.base_row) * p;
 
-        // shift row c of this range (the gathered table; reading it in place from the shard
-        // costs this kernel 16 registers and 1.6% of its bandwidth — measured)
-        const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p : nullptr;
+        // shift row c of this range: the precomputed table, or the range's first row in place
+        const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p
+                             : (job.shift_from_base ? job.base + (rs - job.base_row) * p : nullptr);
         double c[NB];
 #pragma unroll
         for (int J = 0; J < NB; ++J) {

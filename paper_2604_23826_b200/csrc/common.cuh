@@ -30,8 +30,7 @@ struct TileJob {
     const uint64_t* range_start;   // [n_ranges] absolute first row of each local range
     const uint64_t* range_count;   // [n_ranges]
     const uint64_t* tile_prefix;   // [n_ranges + 1] local range r owns tiles [prefix[r], prefix[r+1])
-    const double* shift;           // [n_ranges][p] first row of each range, or nullptr (see below)
-    uint32_t shift_from_base;      // shift == nullptr: 1 = c is the range's first row read from base
+    const double* shift;           // [n_ranges][p] first row of each range, or nullptr (no shift)
     uint32_t n_ranges;
     uint32_t p;
     uint64_t tile_begin, tile_end; // tiles of this launch

@@ -100,6 +100,14 @@ struct sstat_cuda_ctx {
     std::vector<HostBuf> bounce;
     std::vector<cudaEvent_t> ev_copied, ev_free;
     cudaEvent_t ev[6] = {};
+    // per-call state kept across calls: the last uploaded plan (skip identical re-uploads)
+    // and whether the rank header / range flags are still in their reset state
+    std::vector<uint64_t> meta_last;
+    const void* meta_ptr = nullptr;
+    bool flags_clean = false;
+    const void* clean_rank = nullptr;
+    const void* clean_flags = nullptr;
+    uint64_t clean_len = 0;
 };
 
 namespace {
@@ -443,13 +451,28 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     uint64_t* d_starts = c->d_meta.as<uint64_t>();
     uint64_t* d_counts = d_starts + L;
     uint64_t* d_prefix = d_starts + 2 * L;
-    CUDA_TRY(cudaMemcpyAsync(d_starts, hm, (3 * L + 1) * 8, cudaMemcpyHostToDevice, s));
+    const bool same_plan = c->meta_ptr == c->d_meta.p && c->meta_last.size() == 3 * L + 1 &&
+                           std::equal(hm, hm + 3 * L + 1, c->meta_last.begin());
+    c->meta_ptr = nullptr;  // re-validated below once the upload is enqueued
+    if (!same_plan) {
+        CUDA_TRY(cudaMemcpyAsync(d_starts, hm, (3 * L + 1) * 8, cudaMemcpyHostToDevice, s));
+        c->meta_last.assign(hm, hm + 3 * L + 1);
+    }
+    c->meta_ptr = c->d_meta.p;
 
     const uint64_t rank_stride = kHdr + P.lmax * E;
     CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
     CUDA_TRY(c->d_flags.reserve(std::max<uint64_t>(L, 1) * 4));
-    CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, kHdr * 8, s));
-    CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
+    // the header (lowest failing range, first non-finite index) and the range flags are only
+    // written when something is flagged: reset them only after such a call or a realloc
+    if (!(c->flags_clean && c->clean_rank == c->d_rank.p && c->clean_flags == c->d_flags.p && L <= c->clean_len)) {
+        CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, kHdr * 8, s));
+        CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
+        c->clean_rank = c->d_rank.p;
+        c->clean_flags = c->d_flags.p;
+        c->clean_len = std::max<uint64_t>(L, 1);
+    }
+    c->flags_clean = false;  // until this call ends with nothing flagged
     double* rank_buf = c->d_rank.as<double>();
     uint32_t* d_flags = c->d_flags.as<uint32_t>();
     if (!refexact) {
@@ -463,15 +486,14 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     // more than the ~40 us the separate K3a/K3b launches cost.
     CUDA_TRY(c->d_result.reserve(E * 8));
 
-    auto tile_job = [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1, bool shift_in_base) {
+    auto tile_job = [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
         TileJob j{};
         j.base = base;
         j.base_row = base_row;
         j.range_start = d_starts;
         j.range_count = d_counts;
         j.tile_prefix = d_prefix;
-        j.shift = shift_in_base ? nullptr : d_shift;
-        j.shift_from_base = shift_in_base ? 1u : 0u;
+        j.shift = d_shift;
         j.n_ranges = (uint32_t)L;
         j.p = p;
         j.tile_begin = t0;
@@ -492,18 +514,16 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
             if (tm) tm->kernel_launches += 1;
         } else {
-            // K1 and K3a read the shift rows in place from the resident shard; K2 takes a table
-            if (shift && wide) {
+            // the shift table: each range's first row, gathered from the resident shard
+            if (shift) {
                 CUDA_TRY(launch_gather_shift(base, base_row, d_starts, d_counts, (uint32_t)L, p, c->d_shift.as<double>(), s));
                 if (tm) tm->kernel_launches += 1;
             }
-            const bool in_place = shift && !wide;
             CUDA_TRY(cudaEventRecord(c->ev[0], s));  // kernel_seconds brackets K1/K2 alone
-            if (nt > 0) tile_job(base, base_row, 0, nt, in_place);
+            if (nt > 0) tile_job(base, base_row, 0, nt);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
-            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, in_place ? nullptr : d_shift,
-                                       in_place ? base : nullptr, base_row, d_starts, (uint32_t)L, p, P.r0, rank_buf,
-                                       d_flags, s));
+            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
+                                       (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
             if (tm) tm->kernel_launches += 2;
         }
         if (world > 1 || P.mode == Mode::Partials) {
@@ -565,7 +585,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             }
             stream_chunks(c, hr, trow, trows,
                           [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
-                              tile_job(base, base_row, t0, t1, false);
+                              tile_job(base, base_row, t0, t1);
                           },
                           tm);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
@@ -603,6 +623,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                                   // scan rows [prow[u0], prow[u1-1]+prows[u1-1]) as a one-range job
                                   uint64_t hmeta[2] = {prow[u0], 0};
                                   for (uint64_t k = u0; k < u1; ++k) hmeta[1] += prows[k];
+                                  c->meta_ptr = nullptr;  // d_meta overwritten: re-upload next call
                                   CUDA_TRY(cudaMemcpyAsync(d_starts, hmeta, 16, cudaMemcpyHostToDevice, s));
                                   CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_starts + 1, 1, p, d_flags,
                                                                  rank_buf, c->sms * 2, s));
@@ -637,15 +658,15 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         fold_buf = c->d_gather.as<double>();
     }
     CUDA_TRY(cudaEventRecord(c->ev[3], s));
+    CUDA_TRY(c->d_result.reserve((E + world * kHdr) * 8));
     CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, refexact,
                                c->d_result.as<double>(), s));
     if (tm) tm->kernel_launches += 1;
     CUDA_TRY(cudaEventRecord(c->ev[4], s));
     CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
     double* hres = c->h_result.as<double>();
-    CUDA_TRY(cudaMemcpyAsync(hres, c->d_result.p, E * 8, cudaMemcpyDeviceToHost, s));
-    for (int q = 0; q < world; ++q)
-        CUDA_TRY(cudaMemcpyAsync(hres + E + q * kHdr, fold_buf + q * rank_stride, kHdr * 8, cudaMemcpyDeviceToHost, s));
+    // result and every rank's header in one read-back (K3b appends the headers)
+    CUDA_TRY(cudaMemcpyAsync(hres, c->d_result.p, (E + world * kHdr) * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
     if (!scanned && world == 1 && L > 0) {
@@ -658,11 +679,15 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             CUDA_TRY(cudaStreamSynchronize(s));
         }
     }
+    bool any_flag = false;
     for (int q = 0; q < world; ++q) {
-        uint64_t lin;
+        uint64_t lin, range;
+        std::memcpy(&range, hres + E + q * kHdr, 8);
         std::memcpy(&lin, hres + E + q * kHdr + 1, 8);
         out.bad_lin = std::min(out.bad_lin, lin);
+        any_flag |= range != kNone;
     }
+    c->flags_clean = !any_flag;
     std::memcpy(result_host, hres, E * 8);
     if (tm) {
         float ms = 0;

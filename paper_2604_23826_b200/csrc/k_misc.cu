@@ -60,7 +60,10 @@ __global__ void k_find_nonfinite(const double* __restrict__ base, uint64_t base_
 __global__ void k_final_fold_seq(const double* __restrict__ buf, uint64_t rank_stride, uint64_t n_ranges, int world,
                                  uint32_t p, uint32_t precision, double* out) {
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (e >= partial_len(p)) return;
+    const uint64_t E = partial_len(p);
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
+        out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
+    if (e >= E) return;
     out[e] = fold_entry(buf, rank_stride, n_ranges, world, p, precision, e);
 }
 
@@ -70,6 +73,8 @@ __global__ void __launch_bounds__(256) k_final_fold_fast(const double* __restric
     __shared__ double sm[256];
     const uint64_t E = partial_len(p);
     const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
+        out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
     const uint64_t e = blockIdx.x * 32ull + le;
     double s = 0.0;
     if (e < E)
