@@ -170,6 +170,34 @@ int sstat_cuda_range_partials(sstat_cuda_ctx* ctx, const sstat_cuda_source* src,
                               uint64_t first_range, uint64_t last_range, uint32_t precision, uint32_t flags,
                               double* partials_out, sstat_cuda_error* err);
 
+/* ---- the passes next to the path ---- */
+
+/* ColumnSumResult (reduce.hpp:148-158). */
+typedef struct {
+    double float_sum;            /* binary64 (or binary32 widened) sum of the column          */
+    int32_t exact_ok;            /* every value integral and |v| < 2^63: exact sum present    */
+    int32_t float_matches_exact; /* double_equals_int128(float_sum, exact)  (util.cpp:47-52)  */
+    int64_t exact_hi;            /* exact sum, two's-complement 128-bit: hi:lo                */
+    uint64_t exact_lo;
+    uint64_t note_row;           /* !exact_ok: absolute row of the first non-integral value   */
+} sstat_column_sum_result;
+
+/* column_sum (reduce.cpp:32-88): the column's float sum plus the exact 128-bit integer sum,
+ * per range then merged in ascending range order — the identifier check against n(n+1)/2.
+ * SSTAT_FLAG_REFEXACT (always for binary32): each range summed sequentially, bit-identical
+ * float_sum.  Column out of range: SSTAT_ERR_INVALID (std::out_of_range). */
+int sstat_cuda_column_sum(sstat_cuda_ctx* ctx, const sstat_cuda_source* src, uint32_t p, uint32_t column,
+                          const uint64_t* range_start, const uint64_t* range_count, uint64_t n_ranges,
+                          uint32_t precision, uint32_t flags, sstat_column_sum_result* out, sstat_cuda_error* err);
+
+/* Centered co-moments over the plan (accumulate_comoments + merge_comoments,
+ * suffstats.cpp:107-159): n, mean[p] and M2 = sum (x - mean)(x - mean)^T packed, per range
+ * from the shifted single-pass moments (c = the range's first row), merged in ascending
+ * range order with the pairwise update. */
+int sstat_cuda_comoments(sstat_cuda_ctx* ctx, const sstat_cuda_source* src, uint32_t p, const uint64_t* range_start,
+                         const uint64_t* range_count, uint64_t n_ranges, uint32_t flags, uint64_t* n_out,
+                         double* mean_out, double* m2_out, sstat_cuda_error* err);
+
 /* ---- host helpers (no device work) ---- */
 
 /* The range fold over gathered per-rank buffers (host memory), the same code the device

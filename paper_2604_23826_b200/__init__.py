@@ -4,6 +4,8 @@ Drop-in for the reference's dataset_suffstats / accumulate_chunk path; see DESIG
 """
 from .sstat import (  # noqa: F401
     Chunk,
+    CoMoments,
+    ColumnSumResult,
     DatasetSchema,
     DeviceError,
     Engine,

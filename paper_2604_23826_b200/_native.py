@@ -51,6 +51,8 @@ EXPORTS = (
     "sstat_cuda_accumulate",
     "sstat_cuda_dataset",
     "sstat_cuda_range_partials",
+    "sstat_cuda_column_sum",
+    "sstat_cuda_comoments",
     "sstat_fold_ranges_host",
     "sstat_plan_partitions",
     "sstat_merge",
@@ -97,6 +99,17 @@ class Source(Structure):
     ]
 
 
+class ColumnSum(Structure):
+    _fields_ = [
+        ("float_sum", c_double),
+        ("exact_ok", c_int),
+        ("float_matches_exact", c_int),
+        ("exact_hi", ctypes.c_int64),
+        ("exact_lo", c_uint64),
+        ("note_row", c_uint64),
+    ]
+
+
 _lib = None
 
 
@@ -138,6 +151,14 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             c_int,
             [c_void_p, P(Source), c_uint32, c_void_p, c_void_p, c_uint64, c_uint64, c_uint64, c_uint32, c_uint32, dp,
              P(Error)],
+        ),
+        "sstat_cuda_column_sum": (
+            c_int,
+            [c_void_p, P(Source), c_uint32, c_uint32, c_void_p, c_void_p, c_uint64, c_uint32, c_uint32, P(ColumnSum),
+             P(Error)],
+        ),
+        "sstat_cuda_comoments": (
+            c_int, [c_void_p, P(Source), c_uint32, c_void_p, c_void_p, c_uint64, c_uint32, u64p, dp, dp, P(Error)]
         ),
         "sstat_fold_ranges_host": (c_int, [dp, c_uint64, c_uint64, c_int, c_uint32, c_uint32, c_uint32, dp]),
         "sstat_plan_partitions": (c_uint64, [c_uint64, c_uint64, c_void_p, c_void_p]),

@@ -92,8 +92,8 @@ struct sstat_cuda_ctx {
     std::mutex mu;
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
-    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags;
-    HostBuf h_meta, h_result, h_shift, h_flags;
+    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags, d_counts, d_aux;
+    HostBuf h_meta, h_result, h_shift, h_flags, h_counts;
     uint32_t n_slots = 4;
     uint64_t slot_bytes = 256ull << 20;
     std::vector<DevBuf> slots;
@@ -265,7 +265,7 @@ void ensure_slots(sstat_cuda_ctx* c, bool need_bounce) {
     }
 }
 
-enum class Mode { Dataset, Chunk, Partials };
+enum class Mode { Dataset, Chunk, Partials, Comoments };
 
 struct Plan {
     Mode mode = Mode::Dataset;
@@ -329,7 +329,8 @@ void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint
 }
 
 void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile& file) {
-    const bool single_chunk = P.mode != Mode::Dataset;
+    const bool whole = P.mode == Mode::Dataset || P.mode == Mode::Comoments;  // dataset-level calls
+    const bool single_chunk = !whole;
     Fail inv{SSTAT_ERR_INVALID, ""};
     if (P.p == 0) {
         inv.msg = "schema: column count must be >= 1";
@@ -370,7 +371,7 @@ void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFil
             inv.msg = "null row pointer";
             throw inv;
         }
-        if (world == 1 && P.mode == Mode::Dataset) {
+        if (world == 1 && whole) {
             const uint64_t ds = src->first_row + src->n_rows;
             if (src->first_row != 0 || ds != P.total) {
                 inv.msg = "run_reduction: partition covers " + std::to_string(P.total) + " rows but dataset has " +
@@ -384,7 +385,7 @@ void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFil
     }
     uint64_t ds_rows = kNone;  // dataset rows when known to this rank
     if (src->kind == SSTAT_SRC_FILE) ds_rows = file.rows;
-    else if (world == 1 && P.mode == Mode::Dataset) ds_rows = src->first_row + src->n_rows;
+    else if (world == 1 && whole) ds_rows = src->first_row + src->n_rows;
     if (P.R > 0 && ds_rows != kNone && P.starts[P.R - 1] + P.counts[P.R - 1] > ds_rows) {
         inv.msg = "partition exceeds the dataset";
         throw inv;
@@ -421,36 +422,23 @@ void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFil
     }
 }
 
-// The engine proper.  Returns the all-rank outcome; throws Fail.
-void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
-         sstat_cuda_timings* tm) {
-    BinFile file;
-    check_plan(c, src, P, file);
-    const int world = P.mode == Mode::Dataset ? c->world : 1;
-    const bool refexact = (P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1;
-    const bool shift = !(P.flags & SSTAT_FLAG_NO_SHIFT) && !refexact;
-    const uint32_t p = P.p;
-    const uint64_t E = P.E, L = P.L;
-    cudaStream_t s = c->stream;
-
-    // ---- local plan → device ----
+// Local ranges [starts | counts | tile prefix] to the device (skipped when identical to the
+// previous call's upload).  Sets P.n_tiles.
+uint64_t* upload_meta(sstat_cuda_ctx* c, Plan& P, uint64_t TR, cudaStream_t s) {
+    const uint64_t L = P.L;
     CUDA_TRY(c->h_meta.reserve((3 * L + 1) * 8));
     uint64_t* hm = c->h_meta.as<uint64_t>();
-    const uint64_t TR = tile_rows_for(p);
-    auto tiles_of = [TR](uint64_t count) { return (count + TR - 1) / TR; };
     uint64_t nt = 0;
     for (uint64_t i = 0; i < L; ++i) {
         hm[i] = P.starts[P.r0 + i];
         hm[L + i] = P.counts[P.r0 + i];
         hm[2 * L + i] = nt;
-        nt += tiles_of(P.counts[P.r0 + i]);
+        nt += (P.counts[P.r0 + i] + TR - 1) / TR;
     }
     hm[3 * L] = nt;
     P.n_tiles = nt;
     CUDA_TRY(c->d_meta.reserve((3 * L + 1) * 8));
     uint64_t* d_starts = c->d_meta.as<uint64_t>();
-    uint64_t* d_counts = d_starts + L;
-    uint64_t* d_prefix = d_starts + 2 * L;
     const bool same_plan = c->meta_ptr == c->d_meta.p && c->meta_last.size() == 3 * L + 1 &&
                            std::equal(hm, hm + 3 * L + 1, c->meta_last.begin());
     c->meta_ptr = nullptr;  // re-validated below once the upload is enqueued
@@ -459,6 +447,29 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         c->meta_last.assign(hm, hm + 3 * L + 1);
     }
     c->meta_ptr = c->d_meta.p;
+    return d_starts;
+}
+
+// The engine proper.  Returns the all-rank outcome; throws Fail.
+void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
+         sstat_cuda_timings* tm) {
+    BinFile file;
+    check_plan(c, src, P, file);
+    const int world = (P.mode == Mode::Dataset || P.mode == Mode::Comoments) ? c->world : 1;
+    const bool comoments = P.mode == Mode::Comoments;  // co-moments always take the shifted fast path
+    const bool refexact = !comoments && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1);
+    const bool shift = !(P.flags & SSTAT_FLAG_NO_SHIFT) && !refexact;
+    const uint32_t p = P.p;
+    const uint64_t E = P.E, L = P.L;
+    cudaStream_t s = c->stream;
+
+    // ---- local plan → device ----
+    const uint64_t TR = tile_rows_for(p);
+    auto tiles_of = [TR](uint64_t count) { return (count + TR - 1) / TR; };
+    uint64_t* d_starts = upload_meta(c, P, TR, s);
+    uint64_t* d_counts = d_starts + L;
+    uint64_t* d_prefix = d_starts + 2 * L;
+    const uint64_t nt = P.n_tiles;
 
     const uint64_t rank_stride = kHdr + P.lmax * E;
     CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
@@ -522,8 +533,12 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             CUDA_TRY(cudaEventRecord(c->ev[0], s));  // kernel_seconds brackets K1/K2 alone
             if (nt > 0) tile_job(base, base_row, 0, nt);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
-            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
-                                       (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
+            if (comoments)
+                CUDA_TRY(launch_comoment_range(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, (uint32_t)L, p,
+                                               rank_buf + kHdr, P.r0, rank_buf, d_flags, s));
+            else
+                CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
+                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
             if (tm) tm->kernel_launches += 2;
         }
         if (world > 1 || P.mode == Mode::Partials) {
@@ -589,8 +604,12 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                           },
                           tm);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
-            CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
-                                       (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
+            if (comoments)
+                CUDA_TRY(launch_comoment_range(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, (uint32_t)L, p,
+                                               rank_buf + kHdr, P.r0, rank_buf, d_flags, s));
+            else
+                CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
+                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
             if (tm) tm->kernel_launches += 1;
         }
         // Non-finite localisation: re-stream only the flagged ranges (error path).
@@ -659,8 +678,18 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     }
     CUDA_TRY(cudaEventRecord(c->ev[3], s));
     CUDA_TRY(c->d_result.reserve((E + world * kHdr) * 8));
-    CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, refexact,
-                               c->d_result.as<double>(), s));
+    if (comoments) {
+        // every range's count (the merge weights), for all ranks' ranges
+        CUDA_TRY(c->h_counts.reserve(std::max<uint64_t>(P.R, 1) * 8));
+        CUDA_TRY(c->d_counts.reserve(std::max<uint64_t>(P.R, 1) * 8));
+        std::memcpy(c->h_counts.p, P.counts, P.R * 8);
+        CUDA_TRY(cudaMemcpyAsync(c->d_counts.p, c->h_counts.p, P.R * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(launch_comoment_merge(fold_buf, rank_stride, P.R, world, c->d_counts.as<uint64_t>(), p,
+                                       c->d_result.as<double>(), s));
+    } else {
+        CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, refexact,
+                                   c->d_result.as<double>(), s));
+    }
     if (tm) tm->kernel_launches += 1;
     CUDA_TRY(cudaEventRecord(c->ev[4], s));
     CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
@@ -701,6 +730,103 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         tm->exchange_seconds += ms * 1e-3;
         tm->n_local_ranges = (uint32_t)L;
     }
+}
+
+// column_sum (reference src/reduce.cpp:32-88) over the plan's ranges; 32-byte partials
+// {float sum, exact lo, exact hi, first non-integral row} per tile / range.
+struct ColResult {
+    double f;
+    uint64_t lo, hi, bad_row;
+};
+
+void run_colsum(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32_t column, ColResult& res) {
+    BinFile file;
+    check_plan(c, src, P, file);
+    if (column >= P.p)
+        throw Fail{SSTAT_ERR_INVALID, "column_sum: column " + std::to_string(column) + " out of range, dataset has " +
+                                          std::to_string(P.p) + " columns"};
+    const int world = c->world;
+    const uint32_t p = P.p;
+    const uint64_t L = P.L;
+    const bool sequential = (P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1;
+    cudaStream_t s = c->stream;
+    uint64_t* d_starts = upload_meta(c, P, kTileRows, s);
+    uint64_t* d_counts = d_starts + L;
+    uint64_t* d_prefix = d_starts + 2 * L;
+    const uint64_t nt = P.n_tiles;
+    const uint64_t stride = 1 + P.lmax;  // in 32-byte partials: header slot + ranges
+    CUDA_TRY(c->d_rank.reserve(stride * 32));
+    CUDA_TRY(c->d_aux.reserve(std::max<uint64_t>(nt, 1) * 32));
+    char* rank_buf = static_cast<char*>(c->d_rank.p);
+    void* range_parts = rank_buf + 32;
+    if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
+        const double* base = static_cast<const double*>(src->ptr);
+        CUDA_TRY(launch_colsum(base, src->first_row, p, column, d_starts, d_counts, d_prefix, (uint32_t)L, 0, nt,
+                               sequential, P.precision, c->d_aux.p, range_parts, c->sms, s));
+        if (!sequential) CUDA_TRY(launch_colsum_range_fold(c->d_aux.p, d_prefix, (uint32_t)L, range_parts, s));
+    } else if (L > 0) {
+        cudaPointerAttributes attr{};
+        bool pinned = false;
+        if (src->kind == SSTAT_SRC_HOST) {
+            if (cudaPointerGetAttributes(&attr, src->ptr) == cudaSuccess) pinned = attr.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+        }
+        HostRows hr{src, src->kind == SSTAT_SRC_FILE ? &file : nullptr, p, pinned};
+        ensure_slots(c, !pinned);
+        cudaEvent_t e0 = c->ev[0];
+        CUDA_TRY(cudaEventRecord(e0, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy, e0, 0));
+        std::vector<uint64_t> urow, urows;
+        if (sequential) {  // units = whole ranges
+            for (uint64_t i = 0; i < L; ++i) {
+                urow.push_back(P.starts[P.r0 + i]);
+                urows.push_back(P.counts[P.r0 + i]);
+            }
+            stream_chunks(c, hr, urow, urows,
+                          [&](const double* base, uint64_t base_row, uint64_t u0, uint64_t u1) {
+                              CUDA_TRY(launch_colsum(base, base_row, p, column, d_starts + u0, d_counts + u0, nullptr,
+                                                     (uint32_t)(u1 - u0), 0, 0, true, P.precision, nullptr,
+                                                     static_cast<char*>(range_parts) + 32 * u0, c->sms, s));
+                          },
+                          nullptr);
+        } else {  // units = tiles
+            for (uint64_t i = 0; i < L; ++i) {
+                const uint64_t rs = P.starts[P.r0 + i], rc = P.counts[P.r0 + i];
+                for (uint64_t q = 0; q * kTileRows < rc; ++q) {
+                    urow.push_back(rs + q * kTileRows);
+                    urows.push_back(std::min<uint64_t>(kTileRows, rc - q * kTileRows));
+                }
+            }
+            stream_chunks(c, hr, urow, urows,
+                          [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
+                              CUDA_TRY(launch_colsum(base, base_row, p, column, d_starts, d_counts, d_prefix,
+                                                     (uint32_t)L, t0, t1, false, P.precision, c->d_aux.p, nullptr,
+                                                     c->sms, s));
+                          },
+                          nullptr);
+            CUDA_TRY(launch_colsum_range_fold(c->d_aux.p, d_prefix, (uint32_t)L, range_parts, s));
+        }
+    }
+    const void* fold_buf = rank_buf;
+    if (world > 1) {
+        CUDA_TRY(c->d_gather.reserve(stride * 32 * world));
+        ncclResult_t r = ncclAllGather(rank_buf, c->d_gather.p, stride * 4, ncclDouble, c->comm, s);
+        if (r != ncclSuccess) throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r)};
+        fold_buf = c->d_gather.p;
+    }
+    CUDA_TRY(c->d_result.reserve(64));
+    CUDA_TRY(launch_colsum_final(fold_buf, stride, P.R, world, P.precision, c->d_result.p, s));
+    CUDA_TRY(c->h_result.reserve(64));
+    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, 32, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::memcpy(&res, c->h_result.p, 32);
+}
+
+// double_equals_int128 (reference src/util.cpp:47-52).
+bool double_equals_i128(double d, __int128 v) {
+    if (!std::isfinite(d) || d != std::trunc(d)) return false;
+    if (std::fabs(d) >= 0x1p127) return false;
+    return static_cast<__int128>(d) == v;
 }
 
 uint64_t range_of_row(const Plan& P, uint64_t row) {
@@ -780,9 +906,10 @@ int sstat_cuda_destroy(sstat_cuda_ctx* c) {
         cudaStreamSynchronize(c->stream);
         cudaStreamSynchronize(c->copy);
         if (c->comm) ncclCommDestroy(c->comm);
-        for (DevBuf* b : {&c->d_meta, &c->d_tiles, &c->d_rank, &c->d_gather, &c->d_shift, &c->d_result, &c->d_flags})
+        for (DevBuf* b : {&c->d_meta, &c->d_tiles, &c->d_rank, &c->d_gather, &c->d_shift, &c->d_result, &c->d_flags,
+                          &c->d_counts, &c->d_aux})
             b->release();
-        for (HostBuf* b : {&c->h_meta, &c->h_result, &c->h_shift, &c->h_flags}) b->release();
+        for (HostBuf* b : {&c->h_meta, &c->h_result, &c->h_shift, &c->h_flags, &c->h_counts}) b->release();
         for (auto& s : c->slots) s.release();
         for (auto& b : c->bounce) b.release();
         for (auto e : c->ev_copied) cudaEventDestroy(e);
@@ -1009,6 +1136,79 @@ int sstat_fold_ranges_host(const double* buf, uint64_t rank_stride, uint64_t n_r
         out[e] = reference_order ? fold_entry(buf, rank_stride, n_ranges, world, p, precision, e)
                                  : fold_fast(buf, rank_stride, n_ranges, world, E, e);
     return SSTAT_OK;
+}
+
+int sstat_cuda_column_sum(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t p, uint32_t column,
+                          const uint64_t* range_start, const uint64_t* range_count, uint64_t n_ranges,
+                          uint32_t precision, uint32_t flags, sstat_column_sum_result* out, sstat_cuda_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!c || !src || !out) return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
+    try {
+        Guard g(c);
+        if (c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
+        Plan P{};
+        P.p = p;
+        P.precision = precision;
+        P.flags = flags;
+        P.R = n_ranges;
+        P.starts = range_start;
+        P.counts = range_count;
+        ColResult r{};
+        run_colsum(c, src, P, column, r);
+        const __int128 exact = (__int128)(((unsigned __int128)r.hi << 64) | r.lo);
+        out->float_sum = r.f;
+        out->exact_ok = r.bad_row == kNone;
+        out->exact_hi = (int64_t)r.hi;
+        out->exact_lo = r.lo;
+        out->note_row = r.bad_row;
+        out->float_matches_exact = out->exact_ok && double_equals_i128(r.f, exact);
+        return SSTAT_OK;
+    } catch (const Fail& f) {
+        cudaGetLastError();
+        return report(err, f);
+    } catch (const std::exception& e) {
+        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
+    }
+}
+
+int sstat_cuda_comoments(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t p, const uint64_t* range_start,
+                         const uint64_t* range_count, uint64_t n_ranges, uint32_t flags, uint64_t* n_out,
+                         double* mean_out, double* m2_out, sstat_cuda_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!c || !src || !n_out || !mean_out || !m2_out) return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
+    try {
+        Guard g(c);
+        if (c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
+        Plan P{};
+        P.mode = Mode::Comoments;
+        P.p = p;
+        P.precision = 0;
+        P.flags = flags & ~SSTAT_FLAG_REFEXACT;
+        P.R = n_ranges;
+        P.starts = range_start;
+        P.counts = range_count;
+        std::vector<double> result(partial_len(p ? p : 1));
+        Outcome o;
+        run(c, src, P, result.data(), o, nullptr);
+        if (o.bad_lin != kNone) {
+            Fail f{SSTAT_ERR_NONFINITE, ""};
+            f.row = o.bad_lin / p;
+            f.col = (uint32_t)(o.bad_lin % p);
+            f.range = range_of_row(P, f.row);
+            f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
+                    ", column " + std::to_string(f.col);
+            throw f;
+        }
+        *n_out = P.total;
+        std::memcpy(mean_out, result.data(), p * 8);
+        std::memcpy(m2_out, result.data() + p, (partial_len(p) - p) * 8);
+        return SSTAT_OK;
+    } catch (const Fail& f) {
+        cudaGetLastError();
+        return report(err, f);
+    } catch (const std::exception& e) {
+        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
+    }
 }
 
 uint64_t sstat_plan_partitions(uint64_t n_rows, uint64_t chunk_rows, uint64_t* starts, uint64_t* counts) {

@@ -55,4 +55,22 @@ cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_
 cudaError_t launch_generate(double* dst, uint32_t kind, uint64_t seed, double mu, uint32_t n_int, uint64_t first_row,
                             uint64_t n_rows, uint32_t p, cudaStream_t stream);
 
+// ---- column_sum (reduce.cpp:32-88): 32-byte partials {f64/f32 sum, exact lo, exact hi,
+// first non-integral row}; tiles -> ranges -> one ascending final fold ----
+cudaError_t launch_colsum(const double* base, uint64_t base_row, uint32_t p, uint32_t column,
+                          const uint64_t* range_start, const uint64_t* range_count, const uint64_t* tile_prefix,
+                          uint32_t n_ranges, uint64_t tile_begin, uint64_t tile_end, bool sequential,
+                          uint32_t precision, void* tile_parts, void* range_parts, int sms, cudaStream_t stream);
+cudaError_t launch_colsum_range_fold(const void* tile_parts, const uint64_t* tile_prefix, uint32_t n_ranges,
+                                     void* range_parts, cudaStream_t stream);
+cudaError_t launch_colsum_final(const void* buf, uint64_t rank_stride_parts, uint64_t n_ranges, int world,
+                                uint32_t precision, void* out, cudaStream_t stream);
+
+// ---- co-moments (suffstats.cpp:107-159) from K1's shifted tile partials ----
+cudaError_t launch_comoment_range(const double* tile_partials, const uint64_t* tile_prefix, const uint64_t* range_count,
+                                  const double* shift, uint32_t n_ranges, uint32_t p, double* out, uint64_t first_range,
+                                  double* rank_hdr, uint32_t* flags, cudaStream_t stream);
+cudaError_t launch_comoment_merge(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world,
+                                  const uint64_t* counts, uint32_t p, double* out, cudaStream_t stream);
+
 }  // namespace sstat_b200

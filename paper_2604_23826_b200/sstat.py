@@ -230,6 +230,26 @@ class SuffStats:
 
 
 @dataclass
+class ColumnSumResult:
+    """ColumnSumResult (reduce.hpp:148-158)."""
+
+    float_sum: float
+    exact_sum: Optional[int]
+    float_matches_exact: bool
+    exact_note: Optional[str]
+
+
+@dataclass
+class CoMoments:
+    """Centered co-moments (suffstats.hpp:35-45): n, mean, M2 packed."""
+
+    n: int
+    mean: np.ndarray
+    m2: np.ndarray
+    schema: DatasetSchema
+
+
+@dataclass
 class Chunk:
     """Row-major block of rows (chunk.hpp:13-24); values: numpy array or torch tensor."""
 
@@ -402,6 +422,67 @@ class Engine:
             timings.kernel_launches = tm.kernel_launches
         self.last_timings = tm
         return out
+
+    def _source(self, dataset, p: int, first_row: int, n_rows: Optional[int]):
+        src = N.Source()
+        if isinstance(dataset, (str, os.PathLike)):
+            keep = os.fsencode(os.fspath(dataset))
+            src.kind = N.SRC_FILE
+            src.path = keep
+        else:
+            ptr, keep = self._rows_pointer(dataset, None)
+            src.kind = N.SRC_DEVICE if _is_torch_cuda(dataset) else N.SRC_HOST
+            src.ptr = ptr
+            src.first_row = first_row
+            src.n_rows = n_rows if n_rows is not None else _rows_of(dataset, p)
+        return src, keep
+
+    def column_sum(self, dataset, column: int, plan: ReductionPlan, p: Optional[int] = None, flags: int = 0,
+                   first_row: int = 0, n_rows: Optional[int] = None) -> ColumnSumResult:
+        """column_sum (reduce.cpp:32-88); p = the dataset's column count (files: from the header)."""
+        if p is None:
+            if isinstance(dataset, (str, os.PathLike)):
+                with open(dataset, "rb") as fh:
+                    hdr = fh.read(64)
+                p = int.from_bytes(hdr[20:24], "little") if len(hdr) == 64 else 1
+            else:
+                p = int(dataset.shape[1])
+        src, keep = self._source(dataset, p, first_row, n_rows)
+        starts, counts = plan.partition.arrays()
+        res, err = N.ColumnSum(), N.Error()
+        st = self._lib.sstat_cuda_column_sum(self._ctx, ctypes.byref(src), p, column, starts.ctypes.data,
+                                             counts.ctypes.data, len(starts), int(plan.precision), flags,
+                                             ctypes.byref(res), ctypes.byref(err))
+        del keep
+        if st == N.ERR_INVALID and "out of range" in err.msg.decode():
+            raise IndexError(err.msg.decode())
+        if st != N.OK:
+            _raise(st, err, in_dataset=True)
+        exact = None
+        note = None
+        if res.exact_ok:
+            exact = (res.exact_hi << 64) | res.exact_lo
+        else:
+            note = f"non-integral value at row {res.note_row}; exact sum unavailable"
+        return ColumnSumResult(res.float_sum, exact, bool(res.float_matches_exact), note)
+
+    def comoments(self, dataset, schema: DatasetSchema, plan: ReductionPlan, flags: int = 0, first_row: int = 0,
+                  n_rows: Optional[int] = None) -> "CoMoments":
+        """run_reduction(accumulate_comoments, merge_comoments) over the plan (suffstats.cpp:107-159)."""
+        schema.validate()
+        p = schema.column_count()
+        src, keep = self._source(dataset, p, first_row, n_rows)
+        starts, counts = plan.partition.arrays()
+        n, err = ctypes.c_uint64(), N.Error()
+        mean, m2 = np.zeros(p), np.zeros(p * (p + 1) // 2)
+        dp = ctypes.POINTER(ctypes.c_double)
+        st = self._lib.sstat_cuda_comoments(self._ctx, ctypes.byref(src), p, starts.ctypes.data, counts.ctypes.data,
+                                            len(starts), flags, ctypes.byref(n), mean.ctypes.data_as(dp),
+                                            m2.ctypes.data_as(dp), ctypes.byref(err))
+        del keep
+        if st != N.OK:
+            _raise(st, err, in_dataset=True)
+        return CoMoments(n.value, mean, m2, schema)
 
     def generate(self, dst, kind: int, seed: int, mu: float, n_int: int, first_row: int, n_rows: int, p: int) -> None:
         """Fill a CUDA tensor with synthetic rows (bit-identical to oracle_generate)."""
