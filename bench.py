@@ -298,18 +298,29 @@ def run_ours(args):
 
     if rank == 0:
         peak, peak_src = peaks()
+        # dram bytes per launch of the dominant kernel from the committed ncu --set full capture
+        # of this workload (profiles/traffic.json; written by tools/summarize_profiles.py)
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tr = json.load(f)
+            key = {"c2": "k_smallp", "c5": "k_widep"}.get(args.config) if world == 1 else None
+            if key in tr:
+                traffic = tr[key]["dram_read_bytes"] + tr[key]["dram_write_bytes"]
+        except Exception:
+            traffic = None
         bytes_per_launch = local_rows * p * 8
         achieved = bytes_per_launch / kern_s / 1e9
         if p > 64:  # compute-bound: FP64 tensor-pipe roofline, p(p+2) flops per row
             flops = local_rows * p * (p + 2)
             roof = {"bound": "tensor", "achieved": flops / kern_s / 1e12, "peak": DMMA_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": flops / kern_s / 1e12 / DMMA_PEAK_TFLOPS, "traffic": None,
+                    "unit": "TFLOP/s", "frac": flops / kern_s / 1e12 / DMMA_PEAK_TFLOPS, "traffic": traffic,
                     "kernel": "k_widep (K2)", "per_launch_flops": flops, "per_launch_ms": kern_s * 1e3,
                     "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_probe.log; MEASURED_PEAKS.json "
                                    "has no FP64 entry)", "hbm_gb_per_s": achieved}
         else:
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": None,
+                    "frac": achieved / peak, "traffic": traffic,
                     "kernel": f"k_smallp<{(p + 7) // 8},{str(p % 16 == 0).lower()}> (K1)",
                     "per_launch_bytes": bytes_per_launch, "per_launch_ms": kern_s * 1e3, "peak_source": peak_src}
         line = {

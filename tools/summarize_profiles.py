@@ -49,6 +49,20 @@ def full(path):
     return "\n".join(out)
 
 
+def traffic(rep):
+    """dram read/write bytes of the captured launch (for bench.py's roofline.traffic)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+    def get(name):
+        i = hdr.index(name)
+        return float(vals[i].replace(",", "")) * scale[units[i]]
+
+    return {"dram_read_bytes": get("dram__bytes_read.sum"), "dram_write_bytes": get("dram__bytes_write.sum")}
+
+
 if __name__ == "__main__":
     tag, lc, rep = sys.argv[1:4]
     with open(f"profiles/{tag}_launches.md", "w") as f:
