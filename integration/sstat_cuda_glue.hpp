@@ -13,6 +13,9 @@
 //   dataset_suffstats  src/suffstats.cpp:279-288    sstat::cuda::dataset_suffstats
 //   run_reduction's per_chunk callable              sstat::cuda::per_chunk(engine, schema, precision)
 //     include/sstat/reduce.hpp:70-146
+//   column_sum         src/reduce.cpp:32-88         sstat::cuda::column_sum
+//   accumulate_comoments + merge_comoments          sstat::cuda::dataset_comoments
+//     src/suffstats.cpp:107-159
 //
 // Requires the reference headers (include/sstat) and include/sstat_cuda.h; link with
 // -lsstat_b200.  See INTEGRATION.md.
@@ -25,6 +28,7 @@
 #include <string>
 #include <vector>
 
+#include "sstat/binfile.hpp"
 #include "sstat/chunk.hpp"
 #include "sstat/errors.hpp"
 #include "sstat/reduce.hpp"
@@ -187,6 +191,70 @@ inline SuffStats dataset_suffstats(Engine& eng, const double* rows, std::uint64_
     if (st != SSTAT_OK) detail::rethrow(st, err, true);
     fill_timings(timings, t);
     return detail::make_result(schema, plan.precision, n, sums, cross);
+}
+
+namespace detail {
+inline std::vector<std::uint64_t> starts_of(const ReductionPlan& plan) {
+    std::vector<std::uint64_t> v;
+    for (const auto& r : plan.partition.ranges) v.push_back(r.start_row);
+    return v;
+}
+inline std::vector<std::uint64_t> counts_of(const ReductionPlan& plan) {
+    std::vector<std::uint64_t> v;
+    for (const auto& r : plan.partition.ranges) v.push_back(r.row_count);
+    return v;
+}
+}  // namespace detail
+
+/// column_sum over an SSTATBIN file (reduce.cpp:32-88), same result type.
+inline ColumnSumResult column_sum(Engine& eng, const std::filesystem::path& dataset, std::size_t column,
+                                  const ReductionPlan& plan, std::uint32_t flags = 0) {
+    const std::string path = dataset.string();
+    // the column count comes from the file header (binfile.hpp:17-29)
+    BinaryReader probe(dataset);
+    if (column >= probe.columns())
+        throw std::out_of_range("column_sum: column " + std::to_string(column) + " out of range, dataset has " +
+                                std::to_string(probe.columns()) + " columns");
+    const auto starts = detail::starts_of(plan), counts = detail::counts_of(plan);
+    sstat_cuda_source src{};
+    src.kind = SSTAT_SRC_FILE;
+    src.path = path.c_str();
+    sstat_column_sum_result r{};
+    sstat_cuda_error err{};
+    const int st = sstat_cuda_column_sum(eng.get(), &src, probe.columns(), static_cast<std::uint32_t>(column),
+                                         starts.data(), counts.data(), starts.size(),
+                                         static_cast<std::uint32_t>(plan.precision), flags, &r, &err);
+    if (st != SSTAT_OK) detail::rethrow(st, err, true);
+    ColumnSumResult out;
+    out.float_sum = r.float_sum;
+    if (r.exact_ok) {
+        out.exact_sum = static_cast<int128>((static_cast<unsigned __int128>(static_cast<std::uint64_t>(r.exact_hi)) << 64) |
+                                            r.exact_lo);
+        out.float_matches_exact = r.float_matches_exact != 0;
+    } else {
+        out.exact_note = "non-integral value at row " + std::to_string(r.note_row) + "; exact sum unavailable";
+    }
+    return out;
+}
+
+/// run_reduction(accumulate_comoments, merge_comoments) over an SSTATBIN file.
+inline CoMoments dataset_comoments(Engine& eng, const std::filesystem::path& dataset, const DatasetSchema& schema,
+                                   const ReductionPlan& plan) {
+    schema.validate();
+    const std::uint32_t p = static_cast<std::uint32_t>(schema.column_count());
+    const std::string path = dataset.string();
+    const auto starts = detail::starts_of(plan), counts = detail::counts_of(plan);
+    sstat_cuda_source src{};
+    src.kind = SSTAT_SRC_FILE;
+    src.path = path.c_str();
+    CoMoments cm = CoMoments::empty(schema);
+    std::uint64_t n = 0;
+    sstat_cuda_error err{};
+    const int st = sstat_cuda_comoments(eng.get(), &src, p, starts.data(), counts.data(), starts.size(), 0, &n,
+                                        cm.mean.data(), cm.m2.data(), &err);
+    if (st != SSTAT_OK) detail::rethrow(st, err, true);
+    cm.n = n;
+    return cm;
 }
 
 }  // namespace sstat::cuda

@@ -164,6 +164,35 @@ int main() {
         CHECK(threw);
     }
 
+    // 6. column_sum through the glue (reduce.cpp:32-88): identifier column of Table1
+    {
+        const auto cs_cpu = column_sum(bin, 0, plan);
+        const auto cs_gpu = cuda::column_sum(eng, bin, 0, plan, SSTAT_FLAG_REFEXACT);
+        CHECK(cs_cpu.exact_sum.has_value() && cs_gpu.exact_sum.has_value());
+        CHECK(*cs_gpu.exact_sum == *cs_cpu.exact_sum);
+        CHECK(*cs_gpu.exact_sum == static_cast<int128>(n) * (n + 1) / 2);
+        CHECK(cs_gpu.float_sum == cs_cpu.float_sum && cs_gpu.float_matches_exact == cs_cpu.float_matches_exact);
+        const auto frac_cpu = column_sum(bin, 9, plan);  // J = |tan(d)| is not integral
+        const auto frac_gpu = cuda::column_sum(eng, bin, 9, plan);
+        CHECK(!frac_gpu.exact_sum && frac_gpu.exact_note == frac_cpu.exact_note);
+    }
+
+    // 7. co-moments (run_reduction of accumulate_comoments / merge_comoments) vs the CPU
+    {
+        auto per = [&](const Chunk& ch) { return accumulate_comoments(ch, schema); };
+        auto mrg = [](CoMoments a, CoMoments b) { return merge_comoments(std::move(a), b); };
+        const CoMoments cm_cpu = run_reduction(bin, plan, per, mrg, CoMoments::empty(schema));
+        const CoMoments cm_gpu = cuda::dataset_comoments(eng, bin, schema, plan);
+        CHECK(cm_gpu.n == cm_cpu.n);
+        double worst = 0;
+        for (std::size_t j = 0; j < 11; ++j)
+            for (std::size_t k = j; k < 11; ++k) {
+                const double sc = std::sqrt(cm_cpu.m2.at(j, j) * cm_cpu.m2.at(k, k));
+                worst = std::max(worst, std::fabs(cm_gpu.m2.at(j, k) - cm_cpu.m2.at(j, k)) / sc);
+            }
+        CHECK(worst <= 1e-12);
+    }
+
     // 5. sidecar round trip of the GPU result
     auto side = dir / "gpu.ssf";
     save_suffstats(gpu, side);
