@@ -6,24 +6,30 @@
 // consumer warp owns one rectangle and runs the same straight-line program for every
 // rectangle — 16 DMMA per k-step over 8 operand fragments, no per-block predicates (blocks
 // past p multiply zero fragments; a diagonal rectangle's 6 mirrored blocks are computed and
-// dropped), so the warp-synchronous DMMAs are never guarded.  C consumer warps (8 or 4,
-// chosen per p so the rectangles fill them) form a group = one CTA; ceil(items / C) groups
-// cover the triangle, and the groups of a tile run on neighbouring CTAs with equal work.
+// dropped), so the warp-synchronous DMMAs are never guarded.  C consumer warps (4 or 8)
+// form a group = one CTA; G = ceil(items / C) groups cover the triangle.
 //
-// Warp-specialised pipeline, no CTA-wide barrier in the loop:
-//   * producer warp: one elected lane streams each stage of stage_rows rows into a ring of
-//     kStages shared-memory slots with TMA bulk copies (cp.async.bulk, one per row, rows
-//     padded to pitch = 4 mod 16 doubles so the 4-row fragment reads are conflict-free),
-//     completing on the slot's `full` mbarrier (expect_tx); odd p uses 8-byte cp.async from
-//     all 32 lanes with cp.async.mbarrier.arrive;
+// The G groups of a tile form one thread-block CLUSTER (split into m equal clusters when
+// G > 16) that streams the tile through shared memory once:
+//   * producer warp of cluster rank k: one elected lane waits until every consumer warp
+//     of the cluster has released the ring slot (`empty`, K x C arrivals), then issues the
+//     stage's rows rr = k (mod K) as TMA bulk copies multicast to all K CTAs
+//     (cp.async.bulk ... .multicast::cluster), each completing on the receiving CTA's
+//     `full` mbarrier, which expects the whole stage's bytes (expect_tx by its own
+//     producer).  The tile leaves HBM once and L2 once per cluster instead of once per
+//     group; rows are padded to pitch = 4 mod 16 doubles so the 4-row fragment reads are
+//     conflict-free.  Odd p (8-byte-aligned rows) falls back to per-CTA 8-byte cp.async
+//     with cp.async.mbarrier.arrive;
 //   * consumer warps: wait `full`, read fragments (next k-step's loads in flight while the
 //     current DMMAs issue), subtract the range shift held in registers, DMMA, then arrive on
-//     the slot's `empty` mbarrier; one consumer warp per SMSP already saturates its DMMA
-//     unit (measured, profiles/r01_fp64_probe.log), two hide each other's load gaps.
-// Column sums of rectangle J ride on the warp that owns rectangle (0, J).  Each (tile, group) writes disjoint
-// entries of the tile's canonical partial, so the result is a fixed function of the tile.
+//     the slot's `empty` mbarrier of every CTA of the cluster (mapa + remote arrive).
+// Column sums of rectangle J ride on the warp that owns rectangle (0, J).  Each (tile, group)
+// writes disjoint entries of the tile's canonical partial, so the result is a fixed
+// function of the tile (independent of C, clusters, grid and ring depth).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -32,18 +38,19 @@
 namespace sstat_b200 {
 namespace {
 
-// Consumer warps per CTA (one rectangle each) are 8 or 4: with the producer that is at
-// most 3 warps per SMSP, so the 152-register budget fits the 16K-register SMSP file.
-constexpr int kStages = 4;                    // smem ring depth
-constexpr int kMaxStageRows = 16;
-constexpr int kStageElems = 4096;             // doubles per stage: stage_rows = min(16, 4096/p) & ~3
-constexpr int kMaxItems = 4096;
-__constant__ uint32_t c_items[kMaxItems];     // [group][consumer]: idle<<28 | I<<14 | J
+int sms_of(int device) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n;
+}
 
 constexpr uint32_t kIdle = 1u << 28;
 
 struct WideGeom {
-    uint32_t p, nb, nr, pitch, n_groups, stage_rows, consumers;
+    uint32_t p, nb, nr, pitch, n_groups, consumers, ring;
+    uint32_t csize;          // CTAs per cluster (K)
+    uint32_t cpt;            // clusters per tile (m); n_groups == K * m
+    const uint32_t* items;   // device [n_groups][consumers]: idle<<28 | I<<14 | J
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
@@ -55,10 +62,30 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+// arrive on the barrier at the same smem offset in cluster CTA `cta`
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n"
+        ".reg .b32 ra;\n"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// producer side of `empty`: the arrivals come from other CTAs' consumers
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -75,11 +102,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
 }
 
 // Canonical writes of one 8x8 block (column blocks A <= B) from lane (g, kk).
@@ -96,222 +139,378 @@ __device__ __forceinline__ void write_block(double* out, uint32_t p, uint32_t A,
 
 struct UnitInfo {
     uint64_t t;
-    uint32_t grp, r, rows;
+    uint32_t r, rows;
     const double* tile;
 };
 
 __device__ __forceinline__ UnitInfo unit_info(const TileJob& job, const WideGeom& geo, uint32_t tile_rows,
-                                              uint64_t u) {
+                                              uint64_t t) {
     UnitInfo ui;
-    ui.t = job.tile_begin + u / geo.n_groups;
-    ui.grp = (uint32_t)(u % geo.n_groups);
-    ui.r = range_of_tile(job.tile_prefix, job.n_ranges, ui.t);
+    ui.t = t;
+    ui.r = range_of_tile(job.tile_prefix, job.n_ranges, t);
     const uint64_t rs = __ldg(job.range_start + ui.r), rc = __ldg(job.range_count + ui.r);
-    const uint64_t row0 = rs + (ui.t - __ldg(job.tile_prefix + ui.r)) * tile_rows;
+    const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + ui.r)) * tile_rows;
     const uint64_t left = rs + rc - row0;
     ui.rows = left < tile_rows ? (uint32_t)left : tile_rows;
     ui.tile = job.base + (row0 - job.base_row) * geo.p;
     return ui;
 }
 
-__global__ void __maxnreg__(152) k_widep(TileJob job, WideGeom geo, uint32_t tile_rows) {
-    extern __shared__ __align__(128) double sm[];  // kStages x (stage_rows x pitch) | full[kStages] | empty[kStages]
-    const uint32_t p = geo.p, pitch = geo.pitch, nb = geo.nb, srows = geo.stage_rows;
-    const uint32_t slot_elems = srows * pitch;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * slot_elems);
-    uint64_t* empty = full + kStages;
+// One k-step: 4 rows of the stage at `st` (lane kk reads row kk) for the 8 fragments.
+__device__ __forceinline__ void load_frags(double (&r)[8], const double* st, int colI, int colJ) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) r[a] = st[a < 4 ? colI + 8 * a : colJ + 8 * (a - 4)];
+}
+__device__ __forceinline__ void kstep(double (&acc)[16][2], double (&sums)[4], double (&r)[8],
+                                      const double (&cw)[8]) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) r[a] -= cw[a];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) sums[a] += r[4 + a];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a * 4 + b][0], acc[a * 4 + b][1], r[a], r[4 + b]);
+}
+
+// SROWS = rows per ring stage (compile-time, so a stage is one straight-line program with
+// the next k-step's fragment loads issued under the current k-step's DMMAs).  Launched with
+// cluster dimension geo.csize (1 = no cluster).
+template <int SROWS>
+__global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t tile_rows) {
+    extern __shared__ __align__(128) double sm[];  // ring x (SROWS x pitch) | full[ring] | empty[ring]
+    const uint32_t p = geo.p, pitch = geo.pitch, nb = geo.nb, ring = geo.ring, K = geo.csize;
+    const uint32_t slot_elems = SROWS * pitch;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ring * slot_elems);
+    uint64_t* empty = full + ring;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t consumers = geo.consumers;
-    const uint64_t units = (job.tile_end - job.tile_begin) * geo.n_groups;
     const bool bulk = (p % 2 == 0) && (reinterpret_cast<uintptr_t>(job.base) % 16 == 0);
+    // unit u = (tile u / m, cluster part u % m) covers groups [(u % m) K, (u % m + 1) K) of
+    // the tile; cluster c (K consecutive CTAs) runs units c, c + n_clusters, ... so the m
+    // parts of a tile start side by side
+    const uint32_t rank = K > 1 ? cluster_rank() : 0;
+    const uint32_t m = geo.cpt;
+    const uint64_t units = (job.tile_end - job.tile_begin) * m;
+    const uint64_t u_first = blockIdx.x / K, u_step = gridDim.x / K;
 
     // the column pad [p, pitch) of every slot is never written by the copies: zero it once
-    for (uint32_t i = threadIdx.x; i < kStages * srows * (pitch - p); i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; i < ring * SROWS * (pitch - p); i += blockDim.x) {
         const uint32_t row = i / (pitch - p), col = p + i % (pitch - p);
         sm[row * pitch + col] = 0.0;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (uint32_t s = 0; s < ring; ++s) {
             mbar_init(&full[s], bulk ? 1u : 32u);
-            mbar_init(&empty[s], consumers);
+            mbar_init(&empty[s], consumers * K);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    __syncthreads();
+    // every CTA's barriers are initialised before any peer multicasts into it or arrives on it
+    if (K > 1) cluster_sync_all(); else __syncthreads();
 
+    uint32_t slot = 0, ph = 0;  // ring position, advanced once per stage
     if (warp == (int)consumers) {
         // ---------------- producer ----------------
-        uint32_t n = 0;  // global stage counter (slot = n % kStages, phase = (n / kStages) & 1)
-        for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
-            const UnitInfo ui = unit_info(job, geo, tile_rows, u);
-            const uint32_t n_stages = (ui.rows + srows - 1) / srows;
+        const uint16_t mask = (uint16_t)((1u << K) - 1);
+        for (uint64_t u = u_first; u < units; u += u_step) {
+            const UnitInfo ui = unit_info(job, geo, tile_rows, job.tile_begin + u / m);
+            const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
             const double* crow = job.shift != nullptr ? job.shift + (uint64_t)ui.r * p : nullptr;
-            for (uint32_t sidx = 0; sidx < n_stages; ++sidx, ++n) {
-                const uint32_t slot = n % kStages, ph = (n / kStages) & 1;
-                mbar_wait(&empty[slot], ph ^ 1);
-                const uint32_t r0 = sidx * srows;
-                const uint32_t vrows = ui.rows - r0 < srows ? ui.rows - r0 : srows;
+            for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
+                // all K x C consumer warps of the cluster are done with this slot everywhere
+                mbar_wait_cluster(&empty[slot], ph ^ 1);
+                const uint32_t r0 = sidx * SROWS;
+                const uint32_t vrows = ui.rows - r0 < SROWS ? ui.rows - r0 : SROWS;
                 double* dst = sm + slot * slot_elems;
                 const double* src = ui.tile + (uint64_t)r0 * p;
-                // rows past the tile end hold the shift row, so x - c = 0 there (plain stores,
-                // ordered before the release of this lane's arrive below)
-                for (uint32_t rr = vrows; rr < srows; ++rr)
+                // rows past the tile end hold the shift row, so x - c = 0 there (plain local
+                // stores, ordered before the release of this lane's arrive below)
+                for (uint32_t rr = vrows; rr < SROWS; ++rr)
                     for (uint32_t j = lane; j < p; j += 32) dst[rr * pitch + j] = crow ? crow[j] : 0.0;
                 __syncwarp();
                 if (bulk) {
                     if (lane == 0) {
+                        // this CTA receives every valid row of the stage, from all K producers
                         mbar_arrive_expect_tx(&full[slot], vrows * p * 8);
-                        for (uint32_t rr = 0; rr < vrows; ++rr)
-                            bulk_g2s(dst + rr * pitch, src + (uint64_t)rr * p, p * 8, &full[slot]);
+                        if (K > 1) {
+                            for (uint32_t rr = rank; rr < vrows; rr += K)
+                                bulk_g2s_mc(dst + rr * pitch, src + (uint64_t)rr * p, p * 8, &full[slot], mask);
+                        } else {
+                            for (uint32_t rr = 0; rr < vrows; ++rr)
+                                bulk_g2s(dst + rr * pitch, src + (uint64_t)rr * p, p * 8, &full[slot]);
+                        }
                     }
                 } else {
                     for (uint32_t rr = 0; rr < vrows; ++rr)
                         for (uint32_t j = lane; j < p; j += 32) cp_async8(dst + rr * pitch + j, src + (uint64_t)rr * p + j);
                     cp_async_arrive_noinc(&full[slot]);
                 }
+                if (++slot == ring) slot = 0, ph ^= 1;
             }
         }
-        return;
-    }
+    } else {
+        // ---------------- consumers ----------------
+        const int g = lane >> 2, kk = lane & 3;
+        const uint64_t E = partial_len(p);
+        for (uint64_t u = u_first; u < units; u += u_step) {
+            const UnitInfo ui = unit_info(job, geo, tile_rows, job.tile_begin + u / m);
+            const uint32_t grp = (uint32_t)(u % m) * K + rank;
+            const uint32_t item = __ldg(geo.items + grp * consumers + warp);
+            const bool idle = item & kIdle;
+            const uint32_t I = (item >> 14) & 0x3fff, J = item & 0x3fff;
+            // fragment a reads column colI + 8a (a < 4, rectangle I) or colJ + 8(a-4) (rectangle
+            // J); columns past p read the zero pad with c = 0, rows past the tile end read c
+            const int colI = (int)(32 * I) + g, colJ = (int)(32 * J) + g;
+            const bool sums_here = !idle && I == 0;  // rectangle (0, J) sums rectangle J's columns
+            double cw[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                const int col = a < 4 ? colI + 8 * a : colJ + 8 * (a - 4);
+                cw[a] = (!idle && col < (int)p && job.shift != nullptr) ? job.shift[(uint64_t)ui.r * p + col] : 0.0;
+            }
+            double acc[16][2], sums[4];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sums[i] = 0.0;
 
-    // ---------------- consumers ----------------
-    const int g = lane >> 2, kk = lane & 3;
-    const uint64_t E = partial_len(p);
-    uint32_t n = 0;
-    for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const UnitInfo ui = unit_info(job, geo, tile_rows, u);
-        const uint32_t item = c_items[ui.grp * consumers + warp];
-        const bool idle = item & kIdle;
-        const uint32_t I = (item >> 14) & 0x3fff, J = item & 0x3fff;
-        // fragment a reads column colI + 8a (a < 4, rectangle I) or colJ + 8(a-4) (rectangle J);
-        // columns past p read the zero pad with c = 0, rows past the tile end read c
-        const int colI = (int)(32 * I) + g, colJ = (int)(32 * J) + g;
-        double cw[8];
+            const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
+            for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
+                mbar_wait(&full[slot], ph);
+                if (!idle) {  // an idle (padding) warp of the last group keeps the ring protocol only
+                    const double* st = sm + slot * slot_elems + kk * pitch;
+                    double ra[8], rb[8];
+                    load_frags(ra, st, colI, colJ);
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int col = a < 4 ? colI + 8 * a : colJ + 8 * (a - 4);
-            cw[a] = (!idle && col < (int)p && job.shift != nullptr) ? job.shift[(uint64_t)ui.r * p + col] : 0.0;
-        }
-        const bool sums_here = !idle && I == 0;  // rectangle (0, J) sums the columns of rectangle J
-        double acc[16][2], sums[4];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sums[i] = 0.0;
-
-        const uint32_t n_stages = (ui.rows + srows - 1) / srows;
-        for (uint32_t sidx = 0; sidx < n_stages; ++sidx, ++n) {
-            const uint32_t slot = n % kStages, ph = (n / kStages) & 1;
-            mbar_wait(&full[slot], ph);
-            if (idle) {  // padding warp of the last group: keep the ring protocol, skip the math
+                    for (int q = 0; q < SROWS / 4; q += 2) {
+                        if (q + 1 < SROWS / 4) load_frags(rb, st + 4 * (q + 1) * pitch, colI, colJ);
+                        kstep(acc, sums, ra, cw);
+                        if (q + 2 < SROWS / 4) load_frags(ra, st + 4 * (q + 2) * pitch, colI, colJ);
+                        if (q + 1 < SROWS / 4) kstep(acc, sums, rb, cw);
+                    }
+                }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
-                continue;
+                if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[slot], lane);
+                if (++slot == ring) slot = 0, ph ^= 1;
             }
-            const double* st = sm + slot * slot_elems + kk * pitch;
-            double f[8], raw[8];
-#pragma unroll
-            for (int a = 0; a < 8; ++a) raw[a] = st[a < 4 ? colI + 8 * a : colJ + 8 * (a - 4)];
-#pragma unroll
-            for (int q = 0; q < kMaxStageRows / 4; ++q) {
-                if (4u * q >= srows) break;
-#pragma unroll
-                for (int a = 0; a < 8; ++a) f[a] = raw[a] - cw[a];
-                if (4u * (q + 1) < srows) {  // next k-step's loads in flight under this one's DMMAs
-                    const double* nx = st + 4 * (q + 1) * pitch;
-#pragma unroll
-                    for (int a = 0; a < 8; ++a) raw[a] = nx[a < 4 ? colI + 8 * a : colJ + 8 * (a - 4)];
-                }
-#pragma unroll
-                for (int a = 0; a < 4; ++a) sums[a] += f[4 + a];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a * 4 + b][0], acc[a * 4 + b][1], f[a], f[4 + b]);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
-        }
 
-        // ---- epilogue: disjoint canonical entries of the tile partial ----
-        double* out = job.tile_partials + ui.t * E;
-        if (!idle) {
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const uint32_t A = 4 * I + a, B = 4 * J + b;
-                    if (A <= B && B < nb) write_block(out, p, A, B, g, kk, acc[a * 4 + b]);
-                }
-        }
-        if (sums_here) {
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                sums[a] += __shfl_xor_sync(0xffffffffu, sums[a], 1);
-                sums[a] += __shfl_xor_sync(0xffffffffu, sums[a], 2);
-            }
-            if (kk == 0) {
+            // ---- epilogue: disjoint canonical entries of the tile partial ----
+            double* out = job.tile_partials + ui.t * E;
+            if (!idle) {
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
-                    if (colJ + 8 * a < (int)p) out[colJ + 8 * a] = sums[a];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const uint32_t A = 4 * I + a, B = 4 * J + b;
+                        if (A <= B && B < nb) write_block(out, p, A, B, g, kk, acc[a * 4 + b]);
+                    }
+            }
+            if (sums_here) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    sums[a] += __shfl_xor_sync(0xffffffffu, sums[a], 1);
+                    sums[a] += __shfl_xor_sync(0xffffffffu, sums[a], 2);
+                }
+                if (kk == 0) {
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+                        if (colJ + 8 * a < (int)p) out[colJ + 8 * a] = sums[a];
+                }
             }
         }
     }
+    // no CTA leaves while a peer may still multicast into it or arrive on its barriers
+    if (K > 1) cluster_sync_all();
 }
 
-// Rectangles (I <= J) of the nr x nr rectangle grid, dealt to groups of C consumer warps;
-// C = 8 unless C = 4 leaves markedly fewer idle warps.
-std::vector<uint32_t> make_items(uint32_t nr, uint32_t& n_groups, uint32_t& consumers) {
+// Rectangles (I <= J) of the nr x nr rectangle grid, dealt to n_groups groups of
+// `consumers` warps (the last groups padded with idle warps).
+std::vector<uint32_t> make_items(uint32_t nr, uint32_t consumers, uint32_t n_groups) {
     std::vector<uint32_t> items;
     for (uint32_t I = 0; I < nr; ++I)
         for (uint32_t J = I; J < nr; ++J) items.push_back((I << 14) | J);
-    // 8 consumers per CTA unless 4 saves more than an eighth of the slots: fewer, fuller
-    // groups re-read each tile fewer times
-    uint32_t best = 8, best_slots = (uint32_t)((items.size() + 7) / 8) * 8;
-    const uint32_t slots4 = (uint32_t)((items.size() + 3) / 4) * 4;
-    if (8 * (best_slots - slots4) > best_slots) {
-        best = 4;
-        best_slots = slots4;
-    }
-    consumers = best;
-    n_groups = best_slots / best;
-    while (items.size() < best_slots) items.push_back(kIdle);
+    while (items.size() < (size_t)n_groups * consumers) items.push_back(kIdle);
     return items;
+}
+
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = getenv(name);
+    return v ? (uint32_t)atoi(v) : dflt;
+}
+
+// One launch geometry per (device, p): chosen once from the occupancy calculator, its
+// rectangle table kept on the device for the life of the process.
+struct Plan {
+    int device = -1;
+    uint32_t p = 0, srows = 0, grid_cap = 0;  // grid_cap = clusters in flight
+    size_t smem = 0;
+    WideGeom geo{};
+};
+std::mutex g_plan_mu;
+std::vector<Plan> g_plans;
+
+template <int SROWS>
+cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
+    auto kern = k_widep<SROWS>;
+    const int threads = (int)(geo.consumers + 1) * 32;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    // the opt-in limit only caps what a launch may request; set it once to the maximum so
+    // plans with different rings never invalidate each other
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    // deepest ring (2..4 stages) that keeps the target CTAs per SM (2 for 4-warp groups, so
+    // two groups share an SM's four DMMA units; 1 for 8-warp groups)
+    const int want = geo.consumers == 4 ? 2 : 1;
+    size_t smem = 0;
+    int per_sm = 0;
+    for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", 4); ring >= 2; --ring) {
+        geo.ring = ring;
+        smem = sizeof(double) * ring * SROWS * geo.pitch + 2 * ring * sizeof(uint64_t);
+        if (smem > 227 * 1024) continue;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm >= want) break;
+    }
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+
+    // Cluster size K: every candidate K >= 2 (a tile's groups share its stream through the
+    // multicast; K = 1 only when the tile has one group or SSTAT_WIDEP_NOCLUSTER), scored by
+    // the useful consumer warps it keeps resident = clusters in flight x K x C x the real
+    // share of the groups.  The calculator's cluster placement (GPC sizes) and the idle
+    // padding of K * m groups are what separate the candidates.
+    const uint32_t items = geo.nr * (geo.nr + 1) / 2;
+    const uint32_t groups = (items + geo.consumers - 1) / geo.consumers;
+    const uint32_t kmax = std::min<uint32_t>(env_u32("SSTAT_WIDEP_MAXCLUSTER", 16), groups);
+    const bool nocluster = env_u32("SSTAT_WIDEP_NOCLUSTER", 0) != 0 || groups == 1;
+    uint64_t best_score = 0;
+    WideGeom best = geo;
+    uint32_t best_clusters = 0;
+    for (uint32_t K = nocluster ? 1 : 2; K <= (nocluster ? 1 : kmax); ++K) {
+        WideGeom g = geo;
+        g.csize = K;
+        g.cpt = (groups + K - 1) / K;
+        g.n_groups = g.csize * g.cpt;
+        int clusters = 0;
+        if (K == 1) {
+            clusters = sms_of(device) * std::min(per_sm, want);
+        } else {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = K;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.blockDim = dim3(threads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.gridDim = dim3(K * 64);
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+                (void)cudaGetLastError();
+                continue;
+            }
+        }
+        // useful warps in flight, x n_groups to stay integral
+        const uint64_t score = (uint64_t)clusters * K * items;
+        if (g.n_groups == 0) continue;
+        // compare clusters*K*items/n_groups across candidates without division
+        if (score > 0 && (best_score == 0 || score * best.n_groups > best_score * g.n_groups ||
+                          (score * best.n_groups == best_score * g.n_groups && K > best.csize))) {
+            best_score = score;
+            best = g;
+            best_clusters = (uint32_t)clusters;
+        }
+    }
+    if (best_score == 0) return cudaErrorInvalidConfiguration;
+
+    std::vector<uint32_t> tab = make_items(best.nr, best.consumers, best.n_groups);
+    uint32_t* d_items = nullptr;
+    e = cudaMalloc(&d_items, tab.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(d_items, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    best.items = d_items;
+    out.device = device;
+    out.p = geo.p;
+    out.srows = SROWS;
+    out.grid_cap = best_clusters;
+    out.smem = smem;
+    out.geo = best;
+    if (getenv("SSTAT_DEBUG"))
+        fprintf(stderr, "k_widep<%d>: p=%u C=%u groups=%u/%u cluster=%u x %u ring=%u smem=%zu per_sm=%d clusters=%u\n",
+                SROWS, geo.p, best.consumers, groups, best.n_groups, best.csize, best.cpt, best.ring, smem, per_sm,
+                best_clusters);
+    return cudaSuccess;
+}
+
+template <int SROWS>
+cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream) {
+    const uint64_t tiles = job.tile_end - job.tile_begin;
+    if (tiles == 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.geo.csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3((pl.geo.consumers + 1) * 32);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const uint64_t units = tiles * pl.geo.cpt;
+    cfg.gridDim = dim3((unsigned)(std::min<uint64_t>(units, pl.grid_cap) * pl.geo.csize));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_widep<SROWS>, job, pl.geo, widep_tile_rows(pl.geo.p));
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
 }
 
 }  // namespace
 
 uint32_t widep_tile_rows(uint32_t) { return 32768; }
 
-cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream) {
+cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
     const uint32_t p = job.p;
     if (p > 2048 || p < 2) return cudaErrorInvalidValue;
-    WideGeom geo;
-    geo.p = p;
-    geo.nb = (p + 7) / 8;
-    geo.nr = (geo.nb + 3) / 4;
-    // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank groups,
-    // so each half-warp fragment read is one conflict-free wavefront; rows stay 16-B aligned
-    geo.pitch = ((p + 15) / 16) * 16 + 4;
-    geo.stage_rows = std::min<uint32_t>(kMaxStageRows, (kStageElems / p) & ~3u);
-    if (geo.stage_rows < 4) geo.stage_rows = 4;
-    std::vector<uint32_t> items = make_items(geo.nr, geo.n_groups, geo.consumers);
-    if (items.size() > (size_t)kMaxItems) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemcpyToSymbolAsync(c_items, items.data(), items.size() * 4, 0, cudaMemcpyHostToDevice, stream);
+    int device = 0;
+    cudaError_t e = cudaGetDevice(&device);
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(double) * kStages * geo.stage_rows * geo.pitch + 2 * kStages * sizeof(uint64_t);
-    e = cudaFuncSetAttribute(k_widep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    const int threads = (int)(geo.consumers + 1) * 32;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_widep, threads, smem);
-    if (e != cudaSuccess) return e;
-    const uint64_t units = (job.tile_end - job.tile_begin) * geo.n_groups;
-    const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
-    const uint64_t grid = units < cap ? units : cap;
-    if (grid == 0) return cudaSuccess;
-    k_widep<<<(unsigned)grid, threads, smem, stream>>>(job, geo, widep_tile_rows(p));
-    return cudaGetLastError();
+    // stage height: 16 rows up to p = 256, then 8, then 4 (a stage stays ~33 KB)
+    uint32_t srows = p <= 256 ? 16 : p <= 512 ? 8 : 4;
+    if (p <= 256 && env_u32("SSTAT_WIDEP_SROWS", 16) == 8) srows = 8;
+    const bool tuned = getenv("SSTAT_WIDEP_CONSUMERS") || getenv("SSTAT_WIDEP_NOCLUSTER") ||
+                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS");
+    Plan pl;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        bool found = false;
+        if (!tuned)
+            for (const Plan& q : g_plans)
+                if (q.device == device && q.p == p) pl = q, found = true;
+        if (!found) {
+            WideGeom geo{};
+            geo.p = p;
+            geo.nb = (p + 7) / 8;
+            geo.nr = (geo.nb + 3) / 4;
+            // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank
+            // groups, so each half-warp fragment read is one conflict-free wavefront
+            geo.pitch = ((p + 15) / 16) * 16 + 4;
+            // 4-warp groups (two CTAs per SM) leave at most 3 idle rectangles per tile, 8-warp
+            // groups up to 7 but re-read less; the multicast makes the extra groups cheap
+            const uint32_t items = geo.nr * (geo.nr + 1) / 2;
+            geo.consumers = env_u32("SSTAT_WIDEP_CONSUMERS", items <= 64 ? 4 : 8) == 4 ? 4 : 8;
+            e = srows == 16 ? make_plan<16>(device, geo, pl)
+                : srows == 8 ? make_plan<8>(device, geo, pl)
+                             : make_plan<4>(device, geo, pl);
+            if (e != cudaSuccess) return e;
+            if (!tuned) g_plans.push_back(pl);
+        }
+    }
+    return pl.srows == 16 ? launch_plan<16>(job, pl, stream)
+           : pl.srows == 8 ? launch_plan<8>(job, pl, stream)
+                           : launch_plan<4>(job, pl, stream);
 }
 
 }  // namespace sstat_b200

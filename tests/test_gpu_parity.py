@@ -402,11 +402,13 @@ def test_wide_p_cases(engine, oracle, reference, golden, name):
     assert engine.dataset_suffstats(X, schema(p), plan(g["n"], g["chunk"])).bit_equal(got)
 
 
-@pytest.mark.parametrize("p", [65, 72, 97, 128, 130, 200])
+@pytest.mark.parametrize("p", [65, 72, 97, 128, 130, 200, 256, 300, 513, 1024])
 def test_wide_p_shapes_vs_truth(engine, oracle, p):
-    """Odd / ragged wide p (masked column blocks, 8-byte staging for odd p), ragged ranges."""
+    """Odd / ragged wide p (masked column blocks, 8-byte staging for odd p), ragged ranges;
+    p spans every cluster shape (2..9 CTAs of 4 warps, clusters of 8-warp CTAs, several
+    clusters per tile) and stage height (16 / 8 / 4 rows)."""
     rng = np.random.default_rng(p)
-    n = 70001
+    n = 70001 if p <= 256 else 9001
     X = rng.normal(1.0, 1.0, size=(n, p))
     X[:, 0] = rng.integers(1, 100, size=n)
     X[:, 1] = rng.integers(1, 100, size=n)
@@ -414,6 +416,25 @@ def test_wide_p_shapes_vs_truth(engine, oracle, p):
     got = engine.dataset_suffstats(to_dev(X), schema(p), plan(n, 33333))
     check_against(got, n, ts, tS)
     assert np.array_equal(bits(got.cross[[0, 1, p]]), bits(tS[[0, 1, p]]))  # integer block exact
+
+
+@pytest.mark.parametrize("p", [96, 256, 520])
+def test_wide_p_schedule_invariant(engine, p, monkeypatch):
+    """K2's result is a fixed function of the tile: 4- or 8-warp groups, with or without the
+    cluster multicast, give the same bits."""
+    torch = torch_mod()
+    n = 100003 if p <= 256 else 40001
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 2, 7, 1.5, 0, 0, n, p)
+    pl = plan(n, 30011)
+    base = engine.dataset_suffstats(D, schema(p), pl)
+    for env in ({"SSTAT_WIDEP_CONSUMERS": "8"}, {"SSTAT_WIDEP_CONSUMERS": "4"}, {"SSTAT_WIDEP_NOCLUSTER": "1"}):
+        with monkeypatch.context() as m:
+            for k, v in env.items():
+                m.setenv(k, v)
+            assert engine.dataset_suffstats(D, schema(p), pl).bit_equal(base), env
+    del D
+    torch.cuda.empty_cache()
 
 
 def test_c5_scale_wide(engine):
