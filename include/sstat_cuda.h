@@ -138,6 +138,12 @@ int sstat_cuda_set_stream(sstat_cuda_ctx* ctx, void* cuda_stream);
 /* Host staging for HOST/FILE sources: `slots` device buffers of `slot_bytes` each. */
 int sstat_cuda_set_staging(sstat_cuda_ctx* ctx, uint32_t slots, uint64_t slot_bytes);
 
+/* Host feeder threads for PAGEABLE/FILE sources (the loader of reference
+ * src/binfile.cpp:140-161 BinaryReader::read_rows): each staging slot is filled by
+ * `threads` parallel pread/memcpy workers, so the pass runs at the H2D link rate rather than
+ * one core's copy rate.  0 = min(16, hardware threads).  Does not change any result. */
+int sstat_cuda_set_host_threads(sstat_cuda_ctx* ctx, uint32_t threads);
+
 /* ---- multi-GPU (one process per GPU, rows sharded contiguously by range) ---- */
 /* 128-byte ncclUniqueId, created on rank 0 and broadcast by the host framework. */
 int sstat_cuda_nccl_unique_id(void* id_out, size_t id_bytes);

@@ -45,6 +45,7 @@ EXPORTS = (
     "sstat_cuda_destroy",
     "sstat_cuda_set_stream",
     "sstat_cuda_set_staging",
+    "sstat_cuda_set_host_threads",
     "sstat_cuda_nccl_unique_id",
     "sstat_cuda_comm_init",
     "sstat_shard_ranges",
@@ -135,6 +136,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "sstat_cuda_destroy": (c_int, [c_void_p]),
         "sstat_cuda_set_stream": (c_int, [c_void_p, c_void_p]),
         "sstat_cuda_set_staging": (c_int, [c_void_p, c_uint32, c_uint64]),
+        "sstat_cuda_set_host_threads": (c_int, [c_void_p, c_uint32]),
         "sstat_cuda_nccl_unique_id": (c_int, [c_void_p, c_size_t]),
         "sstat_cuda_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t]),
         "sstat_shard_ranges": (c_int, [c_uint64, c_int, c_int, u64p, u64p]),

@@ -15,11 +15,16 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -83,6 +88,92 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Host feeder threads (the loader half of reference src/binfile.cpp:140-161 read_rows): a
+// staging slot is filled by parallel page-cache reads / memcpys of disjoint row blocks, so
+// the pageable and file sources run at the H2D link rate instead of one core's copy rate.
+// The calling thread takes tasks too; run() returns when every task is done and rethrows
+// the first task exception.
+class FillPool {
+public:
+    explicit FillPool(unsigned threads) {
+        for (unsigned i = 1; i < threads; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~FillPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    unsigned size() const { return (unsigned)th_.size() + 1; }
+    void run(size_t n, const std::function<void(size_t)>& fn) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            next_ = 0;
+            n_ = n;
+            pending_ = n;
+            err_ = nullptr;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+        if (err_) std::rethrow_exception(err_);
+    }
+
+private:
+    void work() {
+        for (;;) {
+            size_t i;
+            const std::function<void(size_t)>* fn;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!fn_ || next_ >= n_) return;
+                i = next_++;
+                fn = fn_;
+            }
+            std::exception_ptr e;
+            try {
+                (*fn)(i);
+            } catch (...) {
+                e = std::current_exception();
+            }
+            std::lock_guard<std::mutex> lk(mu_);
+            if (e && !err_) err_ = e;
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && fn_ && next_ < n_); });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(size_t)>* fn_ = nullptr;
+    size_t next_ = 0, n_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    std::exception_ptr err_;
+};
+
+unsigned default_host_threads() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(16u, hw ? hw : 1u));
+}
+
 }  // namespace
 
 struct sstat_cuda_ctx {
@@ -108,6 +199,9 @@ struct sstat_cuda_ctx {
     const void* clean_rank = nullptr;
     const void* clean_flags = nullptr;
     uint64_t clean_len = 0;
+    // host feeder for pageable / file sources (created on first use)
+    unsigned host_threads = 0;  // 0 = default_host_threads()
+    std::unique_ptr<FillPool> pool;
 };
 
 namespace {
@@ -242,6 +336,18 @@ struct HostRows {
         if (file) read_exact(file->fd, dst, n * p * 8, 64 + row * p * 8);
         else std::memcpy(dst, host_row(row), n * p * 8);
     }
+    // the same, as row blocks of >= 4 MiB spread over the feeder threads
+    void fill_parallel(FillPool& pool, void* dst, uint64_t row, uint64_t n) const {
+        const uint64_t row_bytes = (uint64_t)p * 8;
+        const uint64_t min_rows = std::max<uint64_t>(1, (4ull << 20) / row_bytes);
+        const uint64_t parts = std::max<uint64_t>(1, std::min<uint64_t>(pool.size(), n / min_rows));
+        if (parts == 1) return fill(dst, row, n);
+        const uint64_t per = (n + parts - 1) / parts;
+        pool.run(parts, [&](size_t i) {
+            const uint64_t r0 = i * per, r1 = std::min(n, r0 + per);
+            if (r0 < r1) fill(static_cast<char*>(dst) + r0 * row_bytes, row + r0, r1 - r0);
+        });
+    }
 };
 
 void ensure_slots(sstat_cuda_ctx* c, bool need_bounce) {
@@ -311,7 +417,8 @@ void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint
         } else {
             // the bounce buffer of this slot is reused: its previous copy must be done
             if (chunk >= c->n_slots) CUDA_TRY(cudaEventSynchronize(c->ev_copied[slot]));
-            hr.fill(c->bounce[slot].p, row0, nrows);
+            if (!c->pool) c->pool.reset(new FillPool(c->host_threads ? c->host_threads : default_host_threads()));
+            hr.fill_parallel(*c->pool, c->bounce[slot].p, row0, nrows);
             host_src = c->bounce[slot].p;
         }
         CUDA_TRY(cudaMemcpyAsync(c->slots[slot].p, host_src, bytes, cudaMemcpyHostToDevice, c->copy));
@@ -944,6 +1051,14 @@ int sstat_cuda_set_staging(sstat_cuda_ctx* c, uint32_t slots, uint64_t slot_byte
     c->ev_free.clear();
     c->n_slots = slots;
     c->slot_bytes = slot_bytes & ~(uint64_t)127;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_set_host_threads(sstat_cuda_ctx* c, uint32_t threads) {
+    if (!c || threads > 1024) return SSTAT_ERR_INVALID;
+    Guard g(c);
+    c->host_threads = threads;
+    c->pool.reset();
     return SSTAT_OK;
 }
 

@@ -334,6 +334,10 @@ class Engine:
     def set_staging(self, slots: int, slot_bytes: int) -> None:
         self._check(self._lib.sstat_cuda_set_staging(self._ctx, slots, slot_bytes))
 
+    def set_host_threads(self, threads: int) -> None:
+        """Feeder threads for pageable-host and file sources (0 = default); results unchanged."""
+        self._check(self._lib.sstat_cuda_set_host_threads(self._ctx, threads))
+
     def init_distributed(self, rank: int, world: int, unique_id: Optional[bytes]) -> None:
         """Attach an NCCL communicator (one process per GPU)."""
         buf = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None

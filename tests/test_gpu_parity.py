@@ -327,6 +327,36 @@ def test_streaming_small_slots_bit_identical(engine, oracle):
     e.close()
 
 
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_feeder_threads_bit_identical(engine, tmp_path, threads):
+    """The host feeder (parallel pread / memcpy of row blocks into the staging slots) gives
+    the same bits for any thread count, for pageable and file sources, including slots
+    that do not split evenly and a ragged last chunk."""
+    from paper_2604_23826_b200 import Engine
+
+    torch = torch_mod()
+    n, p = 3_000_017, 13
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 0, 9, 0.0, 2, 0, n, p)
+    H = D.cpu().numpy()
+    path = tmp_path / "feed.bin"
+    hdr = bytearray(64)
+    hdr[0:8] = b"SSTATBIN"
+    hdr[8:12] = (1).to_bytes(4, "little")
+    hdr[12:20] = n.to_bytes(8, "little")
+    hdr[20:24] = p.to_bytes(4, "little")
+    with open(path, "wb") as f:
+        f.write(hdr)
+        H.tofile(f)
+    dev = engine.dataset_suffstats(D, schema(p), plan(n, 1 << 18))
+    e = Engine(0)
+    e.set_staging(3, 40 << 20)
+    e.set_host_threads(threads)
+    assert e.dataset_suffstats(H, schema(p), plan(n, 1 << 18)).bit_equal(dev)
+    assert e.dataset_suffstats(str(path), schema(p), plan(n, 1 << 18)).bit_equal(dev)
+    e.close()
+
+
 def test_c1_full_size(engine, oracle):
     """Config 1: 1e6 x (8 + ID), the ID column excluded downstream.  The reference's own
     sequential sum of id^2 (3.3e17 > 2^53) is 1.1e-12 off the true value, so entries are
