@@ -384,10 +384,15 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
     const uint32_t groups = (items + geo.consumers - 1) / geo.consumers;
     const uint32_t kmax = std::min<uint32_t>(env_u32("SSTAT_WIDEP_MAXCLUSTER", 16), groups);
     const bool nocluster = env_u32("SSTAT_WIDEP_NOCLUSTER", 0) != 0 || groups == 1;
-    uint64_t best_score = 0;
-    WideGeom best = geo;
-    uint32_t best_clusters = 0;
+    struct Cand {
+        WideGeom g;
+        int clusters;
+        double value;  // useful consumer warps resident: clusters x K x C x items / (n_groups C)
+    };
+    std::vector<Cand> cands;
+    const uint32_t kforce = env_u32("SSTAT_WIDEP_CLUSTER", 0);
     for (uint32_t K = nocluster ? 1 : 2; K <= (nocluster ? 1 : kmax); ++K) {
+        if (kforce && K != kforce) continue;
         WideGeom g = geo;
         g.csize = K;
         g.cpt = (groups + K - 1) / K;
@@ -412,18 +417,20 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
                 continue;
             }
         }
-        // useful warps in flight, x n_groups to stay integral
-        const uint64_t score = (uint64_t)clusters * K * items;
-        if (g.n_groups == 0) continue;
-        // compare clusters*K*items/n_groups across candidates without division
-        if (score > 0 && (best_score == 0 || score * best.n_groups > best_score * g.n_groups ||
-                          (score * best.n_groups == best_score * g.n_groups && K > best.csize))) {
-            best_score = score;
-            best = g;
-            best_clusters = (uint32_t)clusters;
-        }
+        if (clusters > 0) cands.push_back({g, clusters, (double)clusters * K * items / g.n_groups});
     }
-    if (best_score == 0) return cudaErrorInvalidConfiguration;
+    if (cands.empty()) return cudaErrorInvalidConfiguration;
+    // the largest cluster within 4% of the best value: fewer clusters per tile means fewer
+    // HBM / L2 re-reads of the tile (one cluster per tile reads it from HBM exactly once)
+    double top = 0;
+    for (const Cand& c : cands) top = std::max(top, c.value);
+    const Cand* pick = nullptr;
+    for (const Cand& c : cands)
+        if (c.value >= 0.96 * top && (!pick || c.g.cpt < pick->g.cpt ||
+                                      (c.g.cpt == pick->g.cpt && c.value > pick->value)))
+            pick = &c;
+    WideGeom best = pick->g;
+    const uint32_t best_clusters = (uint32_t)pick->clusters;
 
     std::vector<uint32_t> tab = make_items(best.nr, best.consumers, best.n_groups);
     uint32_t* d_items = nullptr;
@@ -481,7 +488,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
     uint32_t srows = p <= 256 ? 16 : p <= 512 ? 8 : 4;
     if (p <= 256 && env_u32("SSTAT_WIDEP_SROWS", 16) == 8) srows = 8;
     const bool tuned = getenv("SSTAT_WIDEP_CONSUMERS") || getenv("SSTAT_WIDEP_NOCLUSTER") ||
-                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS");
+                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS");
     Plan pl;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);

@@ -1,2 +1,3 @@
-timeout 600 python -m pytest tests -q -m gpu -x -k "feeder or streaming" 2>&1 | tail -3 > gpurun_out/pytest_feeder.log
-timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo "rc=$?" >> gpurun_out/bench_default.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_widep -s 1 -c 1 \
+    -o gpurun_out/k2_full -f python bench.py --steps 1 --warmup 3 --config c5 --no-cpu --no-e2e > gpurun_out/ncu_k2.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_k2.log
