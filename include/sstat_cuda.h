@@ -37,11 +37,14 @@
  *   SSTAT_ERR_SCHEMA     SchemaMismatchError                             errors.hpp:52-56
  *   SSTAT_ERR_INVALID    std::invalid_argument / std::out_of_range
  *   SSTAT_ERR_IO / _FORMAT  IoError / FormatError (file sources)         errors.hpp:18-30
+ *   SSTAT_ERR_UNSUPPORTED  also: p > 2048 columns outside reference-order mode (the fast
+ *                        path stages whole rows in shared memory)
  *   SSTAT_ERR_CUDA / _NCCL / _OOM / _UNSUPPORTED  device-side failures (no reference
  *                        equivalent; the glue throws sstat::Error).
  *
  * Threading.  A context is bound to one CUDA device and serialises its own calls
- * (internal mutex); distinct contexts are independent.  No global mutable state.
+ * (internal mutex); distinct contexts are independent.  The only process-wide state is
+ * K2's write-once, mutex-guarded launch-geometry cache per (device, p).
  */
 #ifndef SSTAT_CUDA_H
 #define SSTAT_CUDA_H

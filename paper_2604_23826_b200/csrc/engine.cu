@@ -523,7 +523,8 @@ void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFil
                   std::to_string(P.span_end) + ")";
         throw inv;
     }
-    if (P.L > 65535 && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1)) {
+    const bool reference_order = P.mode != Mode::Comoments && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1);
+    if (P.L > 65535 && reference_order) {
         inv.msg = "reference-order mode supports at most 65535 ranges per device";
         throw inv;
     }
@@ -565,6 +566,10 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     const int world = (P.mode == Mode::Dataset || P.mode == Mode::Comoments) ? c->world : 1;
     const bool comoments = P.mode == Mode::Comoments;  // co-moments always take the shifted fast path
     const bool refexact = !comoments && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1);
+    // K2 stages at least one k-step (4 rows) of every column in shared memory, double-buffered
+    if (P.p > kMaxWideP && !refexact)
+        throw Fail{SSTAT_ERR_UNSUPPORTED, "p = " + std::to_string(P.p) + " exceeds the " + std::to_string(kMaxWideP) +
+                                              "-column limit of the fast path (reference-order mode has none)"};
     const bool shift = !(P.flags & SSTAT_FLAG_NO_SHIFT) && !refexact;
     const uint32_t p = P.p;
     const uint64_t E = P.E, L = P.L;

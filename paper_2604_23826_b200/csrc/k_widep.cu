@@ -480,7 +480,7 @@ uint32_t widep_tile_rows(uint32_t) { return 32768; }
 
 cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
     const uint32_t p = job.p;
-    if (p > 2048 || p < 2) return cudaErrorInvalidValue;
+    if (p > kMaxWideP || p < 2) return cudaErrorInvalidValue;
     int device = 0;
     cudaError_t e = cudaGetDevice(&device);
     if (e != cudaSuccess) return e;

@@ -15,6 +15,7 @@ cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream);
 // K2: tiles for p > 64 (smem-staged DMMA SYRK), tiles of widep_tile_rows(p) rows.
 cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream);
 uint32_t widep_tile_rows(uint32_t p);
+constexpr uint32_t kMaxWideP = 2048;  // launch_widep rejects wider rows
 
 // shift[r][j] = first row of local range r (0 when the range is empty).
 cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uint64_t* range_start,

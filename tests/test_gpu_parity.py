@@ -448,6 +448,42 @@ def test_wide_p_shapes_vs_truth(engine, oracle, p):
     assert np.array_equal(bits(got.cross[[0, 1, p]]), bits(tS[[0, 1, p]]))  # integer block exact
 
 
+def test_every_p_up_to_72(engine):
+    """Every width through K1's template instances (column blocks 1..8, vector and scalar
+    loads) and across the K1 -> K2 switch at p = 64 / 65, ragged tiles and ranges: the
+    80-bit truth within tolerance, integer columns bit-exact."""
+    rng = np.random.default_rng(2024)
+    for p in range(1, 73):
+        n = 2003 + 37 * p
+        X = rng.normal(0.5, 2.0, size=(n, p))
+        X[:, : min(2, p)] = rng.integers(-50, 100, size=(n, min(2, p)))
+        ts, tS = truth_suffstats(X)
+        got = engine.dataset_suffstats(to_dev(X), schema(p), plan(n, 977))
+        check_against(got, n, ts, tS, X)
+
+
+def test_widest_fast_path_and_limit(engine, oracle):
+    """p = 2048 (K2's widest: 4-row stages, many clusters per tile) against the oracle; p = 2049
+    is refused by the fast path with UNSUPPORTED and served by reference-order mode, bit-exact."""
+    from paper_2604_23826_b200 import DeviceError
+
+    rng = np.random.default_rng(7)
+    n, p = 1500, 2048
+    X = rng.normal(0.0, 1.0, size=(n, p))
+    s0, c0 = oracle.plan_partitions(n, 700)
+    wn, ws, wS = oracle.run_reduction(X, p, s0, c0, 1)
+    got = engine.dataset_suffstats(to_dev(X), schema(p), plan(n, 700))
+    check_against(got, wn, ws, wS)
+    n, p = 40, 2049
+    X = rng.normal(0.0, 1.0, size=(n, p))
+    with pytest.raises(DeviceError, match="2048"):
+        engine.dataset_suffstats(to_dev(X), schema(p), plan(n, 16))
+    s0, c0 = oracle.plan_partitions(n, 16)
+    wn, ws, wS = oracle.run_reduction(X, p, s0, c0, 1)
+    exact = engine.dataset_suffstats(to_dev(X), schema(p), plan(n, 16), flags=2)
+    assert exact.n == wn and np.array_equal(bits(exact.cross), bits(wS)) and np.array_equal(bits(exact.sums), bits(ws))
+
+
 @pytest.mark.parametrize("p", [96, 256, 520])
 def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     """K2's result is a fixed function of the tile: 4- or 8-warp groups, with or without the
