@@ -306,9 +306,20 @@ def run_ours(args):
 
     # ---- e2e: public API from pinned host memory (H2D + result D2H every step) ----
     e2e = None
-    # the e2e leg needs the shard in pinned host memory: only for shards that fit the host comfortably
-    if not args.no_e2e and p <= 64 and local_rows * p * 8 <= 32e9:
-        H = D.cpu().pin_memory()
+    # the e2e leg needs every rank's shard in pinned host memory at once: only when all of them
+    # fit in half the node's RAM (no pageable intermediate copy)
+    shard_bytes = local_rows * p * 8
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        ram = 0
+    fits = ram > 0 and world * shard_bytes <= 0.5 * ram
+    if not args.no_e2e and not fits:
+        e2e = {"unavailable": f"{world} x {shard_bytes / 1e9:.1f} GB pinned shards exceed half of the "
+                              f"{ram / 1e9:.0f} GB host RAM"}
+    if not args.no_e2e and fits and p <= 64 and shard_bytes <= 32e9:
+        H = torch.empty((local_rows, p), dtype=torch.float64, pin_memory=True)
+        H.copy_(D)
         del D
         torch.cuda.empty_cache()
         eng.set_stream(0)

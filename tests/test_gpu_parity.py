@@ -462,6 +462,22 @@ def test_every_p_up_to_72(engine):
         check_against(got, n, ts, tS, X)
 
 
+@pytest.mark.parametrize("p", [16, 32, 256])
+def test_misaligned_device_rows(engine, p):
+    """A device pointer that is only 8-byte aligned (a view one double into a buffer) takes
+    the scalar-load / 8-byte cp.async paths and gives the same bits as an aligned copy."""
+    torch = torch_mod()
+    n = 50_001
+    buf = torch.empty(n * p + 1, dtype=torch.float64, device="cuda")
+    D = buf[1:].view(n, p)
+    assert D.data_ptr() % 16 == 8
+    engine.generate(D, 2, 3, 0.25, 0, 0, n, p)
+    A = D.clone()
+    assert A.data_ptr() % 16 == 0
+    assert engine.dataset_suffstats(D, schema(p), plan(n, 9999)).bit_equal(
+        engine.dataset_suffstats(A, schema(p), plan(n, 9999)))
+
+
 def test_widest_fast_path_and_limit(engine, oracle):
     """p = 2048 (K2's widest: 4-row stages, many clusters per tile) against the oracle; p = 2049
     is refused by the fast path with UNSUPPORTED and served by reference-order mode, bit-exact."""
