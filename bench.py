@@ -52,7 +52,11 @@ CONFIGS = {
 DMMA_PEAK_TFLOPS = 37.03  # measured: profiles/r01_fp64_probe.log (mma.sync m8n8k4 f64, 148 SMs)
 CHUNK_ROWS = 1 << 20
 SEED, MU = 42, 1.0
-CPU_SAMPLE_ROWS = 20_000_000  # reference CPU arm: 2e7 rows x 16 (2.56 GB SSTATBIN in /dev/shm)
+CPU_SAMPLE_BYTES = 2_560_000_000  # reference CPU arm sample: 2.56 GB SSTATBIN in /dev/shm (2e7 rows at p=16)
+
+
+def cpu_sample_rows(p: int) -> int:
+    return CPU_SAMPLE_BYTES // (8 * p)
 
 
 def peaks():
@@ -121,9 +125,12 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def cpu_reference_rows_per_s(steps: int, warmup: int, sample_rows: int = CPU_SAMPLE_ROWS, p: int = 16):
-    """The reference's own dataset_suffstats (oracle/_ref) on an SSTATBIN sample of the C2
-    workload (same generator, same p, chunk 2^20), all host threads.  Returns per-step rows/s."""
+def cpu_reference_rows_per_s(steps: int, warmup: int, config: str = "c2"):
+    """The reference's own dataset_suffstats (oracle/_ref) on a 2.56 GB SSTATBIN sample of the
+    config's workload (same generator, same p, chunk 2^20), all host threads.  Returns
+    (per-step rows/s, threads, (read s, work s), sample rows)."""
+    _, p, kind, n_int, _ = CONFIGS[config]
+    sample_rows = cpu_sample_rows(p)
     import numpy as np
 
     from oracle.oracle import Oracle, Reference
@@ -147,7 +154,7 @@ def cpu_reference_rows_per_s(steps: int, warmup: int, sample_rows: int = CPU_SAM
             from concurrent.futures import ThreadPoolExecutor
 
             def gen(s):
-                return orc.generate(0, SEED, MU, 2, s, min(slab, sample_rows - s), p)
+                return orc.generate(kind, SEED, MU, n_int, s, min(slab, sample_rows - s), p)
 
             with ThreadPoolExecutor(workers) as ex:
                 for arr in ex.map(gen, range(0, sample_rows, slab)):
@@ -163,7 +170,7 @@ def cpu_reference_rows_per_s(steps: int, warmup: int, sample_rows: int = CPU_SAM
             if i >= warmup:
                 rates.append(sample_rows / dt)
                 split = (res[3], res[4])
-        return rates, workers, split
+        return rates, workers, split, sample_rows
     finally:
         try:
             os.remove(path)
@@ -175,20 +182,20 @@ def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    rates, cores, split = cpu_reference_rows_per_s(args.steps, args.warmup)
+    rates, cores, split, sample = cpu_reference_rows_per_s(args.steps, args.warmup, args.config)
     v = statistics.median(rates)
     rows, p, *_ = CONFIGS[args.config]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "rows/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * CPU_SAMPLE_ROWS / v,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sample / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SplitMix64 RowRng generator, bit-identical to the GPU inputs)",
-        "config": {"workload": f"reference CPU dataset_suffstats on a {CPU_SAMPLE_ROWS:.0e}-row sample of "
+        "config": {"workload": f"reference CPU dataset_suffstats on a {sample:.2e}-row sample of "
                                f"{args.config.upper()} (p={p}, chunk_rows 2^20, SSTATBIN in page cache)",
-                   "p": p, "sample_rows": CPU_SAMPLE_ROWS},
+                   "p": p, "sample_rows": sample},
         "gb_per_s": v * 8 * p / 1e9,
         "cpu_baseline": {"value": v, "unit": "rows/s", "cores": cores, "kind": "reference",
-                         "sample": f"{CPU_SAMPLE_ROWS} rows x {p} of the {args.config.upper()} generator, one "
+                         "sample": f"{sample} rows x {p} of the {args.config.upper()} generator, one "
                                    f"dataset_suffstats pass per step, {cores} worker threads; "
                                    f"last step read {split[0]:.2f} s / work {split[1]:.2f} s (summed over workers)"},
         "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -342,10 +349,10 @@ def run_ours(args):
             e2e["file_source"] = e2e_file_source(eng, H, schema, plan, ref_res, k_e2e)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and p == 16:
-        rates, cores, split = cpu_reference_rows_per_s(steps=3, warmup=1)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rates, cores, split, sample = cpu_reference_rows_per_s(steps=3, warmup=1, config=args.config)
         cpu = {"value": statistics.median(rates), "unit": "rows/s", "cores": cores, "kind": "reference",
-               "sample": f"reference dataset_suffstats (oracle/_ref) over {CPU_SAMPLE_ROWS} rows x {p} of the same "
+               "sample": f"reference dataset_suffstats (oracle/_ref) over {sample} rows x {p} of the same "
                          f"generator, chunk_rows 2^20, {cores} worker threads, median of 3 passes"}
 
     if rank == 0:
