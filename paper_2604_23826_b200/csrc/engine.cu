@@ -43,11 +43,13 @@ constexpr uint64_t kNone = ~0ull;
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    uint64_t gen = 0;  // bumped by every (re)allocation: a new allocation may reuse the old address
     cudaError_t reserve(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
+        ++gen;
         const size_t want = std::max<size_t>(n, 256);
         cudaError_t e = cudaMalloc(&p, want);
         if (e == cudaSuccess) cap = want;
@@ -57,6 +59,7 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
+        ++gen;
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
@@ -194,10 +197,10 @@ struct sstat_cuda_ctx {
     // per-call state kept across calls: the last uploaded plan (skip identical re-uploads)
     // and whether the rank header / range flags are still in their reset state
     std::vector<uint64_t> meta_last;
-    const void* meta_ptr = nullptr;
+    uint64_t meta_gen = 0;  // d_meta.gen holding meta_last (0 = none)
     bool flags_clean = false;
-    const void* clean_rank = nullptr;
-    const void* clean_flags = nullptr;
+    uint64_t clean_rank = 0;   // DevBuf::gen of d_rank / d_flags when last reset
+    uint64_t clean_flags = 0;
     uint64_t clean_len = 0;
     // host feeder for pageable / file sources (created on first use)
     unsigned host_threads = 0;  // 0 = default_host_threads()
@@ -547,14 +550,14 @@ uint64_t* upload_meta(sstat_cuda_ctx* c, Plan& P, uint64_t TR, cudaStream_t s) {
     P.n_tiles = nt;
     CUDA_TRY(c->d_meta.reserve((3 * L + 1) * 8));
     uint64_t* d_starts = c->d_meta.as<uint64_t>();
-    const bool same_plan = c->meta_ptr == c->d_meta.p && c->meta_last.size() == 3 * L + 1 &&
+    const bool same_plan = c->meta_gen == c->d_meta.gen && c->meta_last.size() == 3 * L + 1 &&
                            std::equal(hm, hm + 3 * L + 1, c->meta_last.begin());
-    c->meta_ptr = nullptr;  // re-validated below once the upload is enqueued
+    c->meta_gen = 0;  // re-validated below once the upload is enqueued
     if (!same_plan) {
         CUDA_TRY(cudaMemcpyAsync(d_starts, hm, (3 * L + 1) * 8, cudaMemcpyHostToDevice, s));
         c->meta_last.assign(hm, hm + 3 * L + 1);
     }
-    c->meta_ptr = c->d_meta.p;
+    c->meta_gen = c->d_meta.gen;
     return d_starts;
 }
 
@@ -588,11 +591,11 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     CUDA_TRY(c->d_flags.reserve(std::max<uint64_t>(L, 1) * 4));
     // the header (lowest failing range, first non-finite index) and the range flags are only
     // written when something is flagged: reset them only after such a call or a realloc
-    if (!(c->flags_clean && c->clean_rank == c->d_rank.p && c->clean_flags == c->d_flags.p && L <= c->clean_len)) {
+    if (!(c->flags_clean && c->clean_rank == c->d_rank.gen && c->clean_flags == c->d_flags.gen && L <= c->clean_len)) {
         CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, kHdr * 8, s));
         CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
-        c->clean_rank = c->d_rank.p;
-        c->clean_flags = c->d_flags.p;
+        c->clean_rank = c->d_rank.gen;
+        c->clean_flags = c->d_flags.gen;
         c->clean_len = std::max<uint64_t>(L, 1);
     }
     c->flags_clean = false;  // until this call ends with nothing flagged
@@ -754,7 +757,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                                   // scan rows [prow[u0], prow[u1-1]+prows[u1-1]) as a one-range job
                                   uint64_t hmeta[2] = {prow[u0], 0};
                                   for (uint64_t k = u0; k < u1; ++k) hmeta[1] += prows[k];
-                                  c->meta_ptr = nullptr;  // d_meta overwritten: re-upload next call
+                                  c->meta_gen = 0;  // d_meta overwritten: re-upload next call
                                   CUDA_TRY(cudaMemcpyAsync(d_starts, hmeta, 16, cudaMemcpyHostToDevice, s));
                                   CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_starts + 1, 1, p, d_flags,
                                                                  rank_buf, c->sms * 2, s));
