@@ -8,19 +8,28 @@ namespace sstat_b200 {
 // Tile partials come from the previous kernel; read them through L2 (ld.global.cg).
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
-// Lane q of kFoldLanes sums tiles t0+q, t0+q+kFoldLanes, ... of entry e (8 loads in flight).
+// Tile folds of one range run kTileLanes interleaved lanes per entry: lane q sums tiles
+// t0+q, t0+q+kTileLanes, ... (up to 8 loads in flight, masked tails instead of a serial
+// remainder loop), then the lanes are added 0..kTileLanes-1.  A fixed function of the range's
+// tile partials; blocks are kTileLanes x 32 threads.
+constexpr int kTileLanes = 16;
 __device__ __forceinline__ double fold_tiles_lane(const double* __restrict__ tp, uint64_t E, uint64_t e, uint64_t t0,
                                                   uint64_t t1, int q) {
     double s = 0.0;
-    uint64_t t = t0 + q;
-    for (; t + 7 * kFoldLanes < t1; t += 8 * kFoldLanes) {
+    const uint64_t T = t1 - t0;
+    if ((uint64_t)q >= T) return s;
+    const uint32_t cnt = (uint32_t)((T - q + kTileLanes - 1) / kTileLanes);  // this lane's tiles
+    const uint64_t stride = (uint64_t)kTileLanes * E;
+    const double* ptr = tp + (t0 + q) * E + e;
+    for (uint32_t i = 0; i < cnt; i += 8, ptr += 8 * stride) {
+        const uint32_t m = cnt - i;
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = ld_cg(tp + (t + u * kFoldLanes) * E + e);
+        for (int u = 0; u < 8; ++u) v[u] = (uint32_t)u < m ? ld_cg(ptr + u * stride) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+        for (int u = 0; u < 8; ++u)
+            if ((uint32_t)u < m) s += v[u];
     }
-    for (; t < t1; t += kFoldLanes) s += ld_cg(tp + t * E + e);
     return s;
 }
 
@@ -36,14 +45,14 @@ __device__ __forceinline__ void unpack_index(uint32_t p, uint32_t i, uint32_t& j
     k = (uint32_t)(row + ((int64_t)i - start(row)));
 }
 
-// K3a for one local range r, by one block of 256 threads (8 lanes x 32 entries).  The
-// range's tile partials are summed in a fixed order (8 interleaved lanes, then lane 0..7),
+// K3a for one local range r, by one block of kTileLanes x 32 threads.  The range's tile
+// partials are summed in a fixed order (fold_tiles_lane, then lanes 0..kTileLanes-1),
 // and the shifted moments map back to raw moments with c = shift row, n = range rows:
 //   s_j  = s'_j + n c_j
 //   S_jk = S'_jk + c_j s'_k + c_k s'_j + n c_j c_k
 // (exact for integer data below 2^53, like the reference's own sums).  A range whose sums
 // are non-finite is flagged (any non-finite input makes them so; reduce.hpp:111-134 picks
-// the lowest failing range).  sm: (2p + 256) doubles.  c: the shift row (or nullptr = 0).
+// the lowest failing range).  sm: (2p + 32 kTileLanes) doubles.  c: the shift row (or nullptr = 0).
 // Cross entries [p + x0, p + x1) are this block's slice; every slice block folds the p
 // sums (needed for the un-shift) but only slice 0 writes them and flags.
 __device__ inline void fold_range_block(const double* __restrict__ tp, uint64_t t0, uint64_t t1, double n,
@@ -64,7 +73,7 @@ __device__ inline void fold_range_block(const double* __restrict__ tp, uint64_t 
             if (q == 0 && e < hi) {
                 double S = lanes[le];
 #pragma unroll
-                for (int w = 1; w < kFoldLanes; ++w) S += lanes[w * 32 + le];
+                for (int w = 1; w < kTileLanes; ++w) S += lanes[w * 32 + le];
                 if (phase == 0) {
                     const double cj = c ? c[e] : 0.0;
                     ssum[e] = S;

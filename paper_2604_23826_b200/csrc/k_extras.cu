@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "fold.cuh"
 #include "kernels.h"
 
 namespace sstat_b200 {
@@ -167,12 +168,12 @@ __global__ void k_colsum_final(const ColPart* __restrict__ buf, uint64_t rank_st
 // Per local range: mean_j = c_j + s'_j / n, M2_jk = S'_jk - s'_j s'_k / n from the folded
 // shifted moments (tile partials, the same order as K3a).  One block of 256 per range;
 // writes [mean(p) | M2(packed)] and n is implicit (range counts).
-__global__ void __launch_bounds__(256) k_comoment_range(const double* __restrict__ tp,
+__global__ void __launch_bounds__(kTileLanes * 32) k_comoment_range(const double* __restrict__ tp,
                                                         const uint64_t* __restrict__ tile_prefix,
                                                         const uint64_t* __restrict__ range_count,
                                                         const double* __restrict__ shift, uint32_t p, double* out,
                                                         uint64_t first_range, double* rank_hdr, uint32_t* flags) {
-    extern __shared__ double sm[];  // [p] shifted sums, [8][32] lanes
+    extern __shared__ double sm[];  // [p] shifted sums, [kTileLanes][32] lanes
     double* ssum = sm;
     double* lanes = sm + p;
     const uint32_t r = blockIdx.x;
@@ -186,15 +187,11 @@ __global__ void __launch_bounds__(256) k_comoment_range(const double* __restrict
         const uint64_t lo = phase == 0 ? 0 : p, hi = phase == 0 ? p : E;
         for (uint64_t e0 = lo; e0 < hi; e0 += 32) {
             const uint64_t e = e0 + le;
-            double s = 0.0;
-            if (e < hi) {  // fold_tiles_lane order (K3a)
-                for (uint64_t t = t0 + q; t < t1; t += kFoldLanes) s += __ldcg(tp + t * E + e);
-            }
-            lanes[q * 32 + le] = s;
+            lanes[q * 32 + le] = e < hi ? fold_tiles_lane(tp, E, e, t0, t1, q) : 0.0;  // K3a's order
             __syncthreads();
             if (q == 0 && e < hi) {
                 double S = lanes[le];
-                for (int w = 1; w < kFoldLanes; ++w) S += lanes[w * 32 + le];
+                for (int w = 1; w < kTileLanes; ++w) S += lanes[w * 32 + le];
                 if (phase == 0) {
                     ssum[e] = S;
                     const double c = shift ? shift[(uint64_t)r * p + e] : 0.0;
@@ -308,12 +305,12 @@ cudaError_t launch_comoment_range(const double* tile_partials, const uint64_t* t
                                   const double* shift, uint32_t n_ranges, uint32_t p, double* out, uint64_t first_range,
                                   double* rank_hdr, uint32_t* flags, cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
-    const size_t smem = (p + kFoldLanes * 32) * sizeof(double);
+    const size_t smem = (p + kTileLanes * 32) * sizeof(double);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_comoment_range, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_comoment_range<<<n_ranges, 256, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, p, out,
+    k_comoment_range<<<n_ranges, kTileLanes * 32, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, p, out,
                                                       first_range, rank_hdr, flags);
     return cudaGetLastError();
 }

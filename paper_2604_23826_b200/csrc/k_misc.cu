@@ -21,10 +21,10 @@ __global__ void k_gather_shift(const double* __restrict__ base, uint64_t base_ro
     shift[i] = range_count[r] ? base[(range_start[r] - base_row) * p + j] : 0.0;
 }
 
-// K3a: one block (256 threads) per local range (fold_range_block, shared with K1's fused path).
+// K3a: blocks of kTileLanes x 32 threads over (local range, cross-entry slice) (fold_range_block).
 // The shift row comes from the table, or (shift == nullptr, base != nullptr) in place as the
 // range's first row of the resident shard.
-__global__ void __launch_bounds__(256) k_range_fold(const double* __restrict__ tp,
+__global__ void __launch_bounds__(kTileLanes * 32) k_range_fold(const double* __restrict__ tp,
                                                     const uint64_t* __restrict__ tile_prefix,
                                                     const uint64_t* __restrict__ range_count,
                                                     const double* __restrict__ shift, const double* base,
@@ -77,8 +77,17 @@ __global__ void __launch_bounds__(256) k_final_fold_fast(const double* __restric
         out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
     const uint64_t e = blockIdx.x * 32ull + le;
     double s = 0.0;
-    if (e < E)
-        for (uint64_t r = q; r < n_ranges; r += kFoldLanes) s += range_partial(buf, rank_stride, n_ranges, world, E, r)[e];
+    if (e < E) {  // fold_lane's order, four loads in flight ahead of the adds
+        uint64_t r = q;
+        for (; r + 3 * kFoldLanes < n_ranges; r += 4 * kFoldLanes) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcg(range_partial(buf, rank_stride, n_ranges, world, E, r + u * kFoldLanes) + e);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s += v[u];
+        }
+        for (; r < n_ranges; r += kFoldLanes) s += __ldcg(range_partial(buf, rank_stride, n_ranges, world, E, r) + e);
+    }
     sm[q * 32 + le] = s;
     __syncthreads();
     if (q == 0 && e < E) {
@@ -197,7 +206,7 @@ cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_
                               uint32_t n_ranges, uint32_t p, uint64_t first_range, double* rank_buf, uint32_t* flags,
                               cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
-    const size_t smem = (2 * p + kFoldLanes * 32) * sizeof(double);  // fold_range_block scratch
+    const size_t smem = (2 * p + kTileLanes * 32) * sizeof(double);  // fold_range_block scratch
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_range_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -207,7 +216,7 @@ cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_
     const uint64_t cross = (uint64_t)p * (p + 1) / 2;
     const uint64_t slice = 32ull * ((p + 31) / 32);
     const dim3 grid(n_ranges, (unsigned)((cross + slice - 1) / slice));
-    k_range_fold<<<grid, 256, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, base, base_row,
+    k_range_fold<<<grid, kTileLanes * 32, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, base, base_row,
                                               range_start, p, first_range, rank_buf, flags, slice);
     return cudaGetLastError();
 }

@@ -462,6 +462,33 @@ def test_every_p_up_to_72(engine):
         check_against(got, n, ts, tS, X)
 
 
+def test_buffer_growth_sequence():
+    """One context through growing and shrinking widths, a non-finite call in between: the
+    error header and range flags are reset whenever a buffer is reallocated (a new allocation
+    can reuse the old address with fresh, zeroed pages), so clean calls never report stale
+    failures and the failing call reports the right cell."""
+    from paper_2604_23826_b200 import Engine, ReductionError
+
+    torch = torch_mod()
+    e = Engine(0)
+    rng = np.random.default_rng(11)
+    for p, bad in ((16, None), (700, None), (9, (5, 3)), (1024, None), (16, None), (1500, None), (64, (70, 63))):
+        n = 3000
+        X = rng.normal(0.0, 1.0, size=(n, p))
+        if bad:
+            X[bad] = np.nan
+            with pytest.raises(ReductionError, match=f"row {bad[0]}, column {bad[1]}"):
+                e.dataset_suffstats(to_dev(X), schema(p), plan(n, 1000))
+        else:
+            ts, tS = truth_suffstats(X) if p <= 256 else (None, None)
+            got = e.dataset_suffstats(to_dev(X), schema(p), plan(n, 1000))
+            assert got.n == n and np.all(np.isfinite(got.cross))
+            if ts is not None:
+                check_against(got, n, ts, tS)
+    e.close()
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("p", [16, 32, 256])
 def test_misaligned_device_rows(engine, p):
     """A device pointer that is only 8-byte aligned (a view one double into a buffer) takes
