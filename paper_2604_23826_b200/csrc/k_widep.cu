@@ -161,16 +161,37 @@ __device__ __forceinline__ void load_frags(double (&r)[8], const double* st, int
 #pragma unroll
     for (int a = 0; a < 8; ++a) r[a] = st[a < 4 ? colI + 8 * a : colJ + 8 * (a - 4)];
 }
+// DADD shares the FP64 pipe with DMMA (profiles/r01_fp64_mix_probe.log): only the warps that
+// own a rectangle (0, J) add the column sums (SUMS), the others issue 8 DADD per 16 DMMA.
+template <bool SUMS>
 __device__ __forceinline__ void kstep(double (&acc)[16][2], double (&sums)[4], double (&r)[8],
                                       const double (&cw)[8]) {
 #pragma unroll
     for (int a = 0; a < 8; ++a) r[a] -= cw[a];
+    if (SUMS) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) sums[a] += r[4 + a];
+        for (int a = 0; a < 4; ++a) sums[a] += r[4 + a];
+    }
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a * 4 + b][0], acc[a * 4 + b][1], r[a], r[4 + b]);
+}
+
+// One ring stage of SROWS rows: a straight-line program with the next k-step's fragment
+// loads issued under the current k-step's DMMAs.
+template <int SROWS, bool SUMS>
+__device__ __forceinline__ void consume_stage(double (&acc)[16][2], double (&sums)[4], const double* st,
+                                              uint32_t pitch, int colI, int colJ, const double (&cw)[8]) {
+    double ra[8], rb[8];
+    load_frags(ra, st, colI, colJ);
+#pragma unroll
+    for (int q = 0; q < SROWS / 4; q += 2) {
+        if (q + 1 < SROWS / 4) load_frags(rb, st + 4 * (q + 1) * pitch, colI, colJ);
+        kstep<SUMS>(acc, sums, ra, cw);
+        if (q + 2 < SROWS / 4) load_frags(ra, st + 4 * (q + 2) * pitch, colI, colJ);
+        if (q + 1 < SROWS / 4) kstep<SUMS>(acc, sums, rb, cw);
+    }
 }
 
 // SROWS = rows per ring stage (compile-time, so a stage is one straight-line program with
@@ -278,18 +299,12 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
             const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
             for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
                 mbar_wait(&full[slot], ph);
-                if (!idle) {  // an idle (padding) warp of the last group keeps the ring protocol only
-                    const double* st = sm + slot * slot_elems + kk * pitch;
-                    double ra[8], rb[8];
-                    load_frags(ra, st, colI, colJ);
-#pragma unroll
-                    for (int q = 0; q < SROWS / 4; q += 2) {
-                        if (q + 1 < SROWS / 4) load_frags(rb, st + 4 * (q + 1) * pitch, colI, colJ);
-                        kstep(acc, sums, ra, cw);
-                        if (q + 2 < SROWS / 4) load_frags(ra, st + 4 * (q + 2) * pitch, colI, colJ);
-                        if (q + 1 < SROWS / 4) kstep(acc, sums, rb, cw);
-                    }
-                }
+                // an idle (padding) warp of the last group keeps the ring protocol only
+                const double* st = sm + slot * slot_elems + kk * pitch;
+                if (sums_here)
+                    consume_stage<SROWS, true>(acc, sums, st, pitch, colI, colJ, cw);
+                else if (!idle)
+                    consume_stage<SROWS, false>(acc, sums, st, pitch, colI, colJ, cw);
                 __syncwarp();
                 if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[slot], lane);
                 if (++slot == ring) slot = 0, ph ^= 1;

@@ -1,3 +1,2 @@
-timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -4 > gpurun_out/pytest_gpu.log
-timeout 300 python tools/step_profile.py > gpurun_out/step_profile.log 2>&1
-timeout 300 python tools/step_profile.py 1e6 9 >> gpurun_out/step_profile.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x -k "wide or every_p or widest or c5 or misaligned" 2>&1 | tail -3 > gpurun_out/pytest_wide.log
+for i in 1 2; do timeout 300 python bench.py --steps 5 --warmup 3 --config c5 --no-cpu --no-e2e > gpurun_out/bench_c5_$i.log 2>&1; done

@@ -38,6 +38,16 @@ for _ in range(K):
 e1.record(stream)
 torch.cuda.synchronize()
 dev = e0.elapsed_time(e1) / K * 1e-3
+# per-call device interval (event before the call -> event after it) and the gap to the next call
+ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+for a, b in ev:
+    a.record(stream)
+    eng.dataset_suffstats(D, schema, plan)
+    b.record(stream)
+torch.cuda.synchronize()
+inside = statistics.mean(a.elapsed_time(b) for a, b in ev) * 1e3
+gap = statistics.mean(ev[i][1].elapsed_time(ev[i + 1][0]) for i in range(K - 1)) * 1e3
+print(f"  per call on the device {inside:.1f} us (enqueue -> result copied), between calls {gap:.1f} us")
 us = lambda v: f"{statistics.mean(v) * 1e6:8.1f} us"  # noqa: E731
 print(f"rows={n} p={p}  device step {dev * 1e6:8.1f} us | K1 {us(kern)} | folds {us(fold)} | "
       f"library total {us(total)} | python call {us(host)} | device - K1 - folds "
