@@ -377,7 +377,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
     if (e != cudaSuccess) return e;
     // deepest ring (2..4 stages) that keeps the target CTAs per SM (2 for 4-warp groups, so
     // two groups share an SM's four DMMA units; 1 for 8-warp groups)
-    const int want = geo.consumers == 4 ? 2 : 1;
+    const int want = (int)env_u32("SSTAT_WIDEP_PERSM", geo.consumers == 4 ? 2 : 1);
     size_t smem = 0;
     int per_sm = 0;
     for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", 4); ring >= 2; --ring) {
@@ -503,7 +503,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
     uint32_t srows = p <= 256 ? 16 : p <= 512 ? 8 : 4;
     if (p <= 256 && env_u32("SSTAT_WIDEP_SROWS", 16) == 8) srows = 8;
     const bool tuned = getenv("SSTAT_WIDEP_CONSUMERS") || getenv("SSTAT_WIDEP_NOCLUSTER") ||
-                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS");
+                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS") || getenv("SSTAT_WIDEP_PERSM");
     Plan pl;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
