@@ -52,7 +52,8 @@ CONFIGS = {
 DMMA_PEAK_TFLOPS = 37.03  # measured: profiles/r01_fp64_probe.log (mma.sync m8n8k4 f64, 148 SMs)
 CHUNK_ROWS = 1 << 20
 SEED, MU = 42, 1.0
-CPU_SAMPLE_BYTES = 2_560_000_000  # reference CPU arm sample: 2.56 GB SSTATBIN in /dev/shm (2e7 rows at p=16)
+# reference CPU arm sample: 2.56 GB SSTATBIN in /dev/shm (2e7 rows at p=16); the override is for tests
+CPU_SAMPLE_BYTES = int(os.environ.get("SSTAT_BENCH_SAMPLE_BYTES", 2_560_000_000))
 
 
 def cpu_sample_rows(p: int) -> int:
