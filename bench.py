@@ -312,6 +312,38 @@ def run_ours(args):
     kern_s = max_over_ranks(sum(kern) / len(kern))
     value = n_global / (ms * 1e-3)
 
+    # ---- SURVEY §8(f) rows on the same resident shard: column_sum (exact identifier sum)
+    # and co-moments, device-timed like the main pass ----
+    def timed(fn, k):
+        for _ in range(2):
+            fn()
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b) / k * 1e-3)
+
+    next_rows = None
+    if not args.no_next:
+        k_next = max(3, min(args.steps, 10))
+        t_cs = timed(lambda: eng.column_sum(D, 0, plan, p=p, first_row=r0, n_rows=local_rows), k_next)
+        t_cm = timed(lambda: eng.comoments(D, schema, plan, first_row=r0, n_rows=local_rows), k_next)
+        sector_rows = local_rows * min(8 * p, 32)  # bytes: the 32-B sectors holding the column
+        next_rows = {
+            "column_sum": {"value": n_global / t_cs, "unit": "rows/s", "ms_per_step": t_cs * 1e3, "column": 0,
+                           "what": "column_sum (reduce.cpp:32-88): FP64 sum + exact 128-bit integer sum of one column",
+                           "algorithmic_gb_per_s": local_rows * 8 / t_cs / 1e9,
+                           "sector_gb_per_s": sector_rows / t_cs / 1e9,
+                           "note": "row-major rows: one 32-byte DRAM sector per row carries the column"},
+            "comoments": {"value": n_global / t_cm, "unit": "rows/s", "ms_per_step": t_cm * 1e3,
+                          "what": "run_reduction(accumulate_comoments, merge_comoments) (suffstats.cpp:107-159)",
+                          "gb_per_s": local_rows * p * 8 / t_cm / 1e9},
+        }
+
     # ---- e2e: public API from pinned host memory (H2D + result D2H every step) ----
     e2e = None
     # the e2e leg needs every rank's shard in pinned host memory at once: only when all of them
@@ -399,6 +431,7 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
+            "next_rows": next_rows,
         }
         print(json.dumps(line), flush=True)
     eng.close()
@@ -415,6 +448,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the column_sum / co-moment timings")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
