@@ -332,13 +332,14 @@ def run_ours(args):
         k_next = max(3, min(args.steps, 10))
         t_cs = timed(lambda: eng.column_sum(D, 0, plan, p=p, first_row=r0, n_rows=local_rows), k_next)
         t_cm = timed(lambda: eng.comoments(D, schema, plan, first_row=r0, n_rows=local_rows), k_next)
-        sector_rows = local_rows * min(8 * p, 32)  # bytes: the 32-B sectors holding the column
         next_rows = {
             "column_sum": {"value": n_global / t_cs, "unit": "rows/s", "ms_per_step": t_cs * 1e3, "column": 0,
                            "what": "column_sum (reduce.cpp:32-88): FP64 sum + exact 128-bit integer sum of one column",
-                           "algorithmic_gb_per_s": local_rows * 8 / t_cs / 1e9,
-                           "sector_gb_per_s": sector_rows / t_cs / 1e9,
-                           "note": "row-major rows: one 32-byte DRAM sector per row carries the column"},
+                           "column_gb_per_s": local_rows * 8 / t_cs / 1e9,
+                           "row_gb_per_s": local_rows * p * 8 / t_cs / 1e9,
+                           "note": "row-major rows: the memory system moves each row's whole 128-B line for one "
+                                   "8-B column (ncu: 4 L2 sectors per row, DRAM read = all 8p bytes), so the "
+                                   "bound is the row bytes at HBM bandwidth"},
             "comoments": {"value": n_global / t_cm, "unit": "rows/s", "ms_per_step": t_cm * 1e3,
                           "what": "run_reduction(accumulate_comoments, merge_comoments) (suffstats.cpp:107-159)",
                           "gb_per_s": local_rows * p * 8 / t_cm / 1e9},
