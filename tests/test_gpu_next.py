@@ -140,3 +140,21 @@ def test_comoments_vs_reference_and_two_pass(engine, oracle, reference):
     d = np.sqrt(np.outer(np.diag(C), np.diag(C))).astype(np.float64)
     assert np.max(np.abs(M2 - C.astype(np.float64)) / d) <= 1e-12
     assert np.max(np.abs(cm.mean - mu.astype(np.float64))) <= 1e-12 * 1000
+
+
+@pytest.mark.parametrize("p", [80, 256])
+def test_comoments_wide_p(engine, p):
+    """Co-moments through K2 (p > 64): mean 50 data over ragged ranges against an 80-bit
+    two-pass (CS-normalised 1e-12), and the reference's merge order is irrelevant to the bar."""
+    rng = np.random.default_rng(p)
+    n = 60_001
+    Y = 50.0 + rng.normal(size=(n, p))
+    L = Y.astype(np.longdouble)
+    mu = L.mean(axis=0)
+    C = ((L - mu).T @ (L - mu)).astype(np.float64)
+    cm = engine.comoments(to_dev(Y), schema(p), plan(n, 7919))
+    assert cm.n == n
+    iu = np.triu_indices(p)
+    scale = np.sqrt(np.abs(np.diag(C)[iu[0]] * np.diag(C)[iu[1]]))
+    assert np.max(np.abs(cm.m2 - C[iu]) / scale) <= 1e-12
+    assert np.max(np.abs(cm.mean - mu.astype(np.float64)) / np.abs(mu.astype(np.float64))) <= 1e-14

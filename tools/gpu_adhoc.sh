@@ -1,1 +1,1 @@
-timeout 600 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_bytes.sum --clock-control none -k regex:k_colsum_tiles -s 2 -c 1 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_colsum.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_next.py -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest_new.log
