@@ -35,6 +35,7 @@ struct TileJob {
     uint32_t p;
     uint64_t tile_begin, tile_end; // tiles of this launch
     double* tile_partials;         // [n_tiles][partial_len(p)] canonical, shifted space
+    unsigned long long* claim;     // 8-byte device scratch for K2's dynamic work split (or nullptr)
 };
 
 // Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).

@@ -186,7 +186,7 @@ struct sstat_cuda_ctx {
     std::mutex mu;
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
-    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags, d_counts, d_aux;
+    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags, d_counts, d_aux, d_claim;
     HostBuf h_meta, h_result, h_shift, h_flags, h_counts;
     uint32_t n_slots = 4;
     uint64_t slot_bytes = 256ull << 20;
@@ -625,6 +625,10 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         j.tile_begin = t0;
         j.tile_end = t1;
         j.tile_partials = c->d_tiles.as<double>();
+        if (wide) {
+            CUDA_TRY(c->d_claim.reserve(sizeof(unsigned long long)));
+            j.claim = c->d_claim.as<unsigned long long>();
+        }
         CUDA_TRY(wide ? launch_widep(j, c->sms, s) : launch_smallp(j, c->sms, s));
     };
 
@@ -1022,7 +1026,7 @@ int sstat_cuda_destroy(sstat_cuda_ctx* c) {
         cudaStreamSynchronize(c->copy);
         if (c->comm) ncclCommDestroy(c->comm);
         for (DevBuf* b : {&c->d_meta, &c->d_tiles, &c->d_rank, &c->d_gather, &c->d_shift, &c->d_result, &c->d_flags,
-                          &c->d_counts, &c->d_aux})
+                          &c->d_counts, &c->d_aux, &c->d_claim})
             b->release();
         for (HostBuf* b : {&c->h_meta, &c->h_result, &c->h_shift, &c->h_flags, &c->h_counts}) b->release();
         for (auto& s : c->slots) s.release();

@@ -51,6 +51,11 @@ struct WideGeom {
     uint32_t csize;          // CTAs per cluster (K)
     uint32_t cpt;            // clusters per tile (m); n_groups == K * m
     const uint32_t* items;   // device [n_groups][consumers]: idle<<28 | I<<14 | J
+    // dynamic split with a concurrent second launch (nullptr = static unit order): both
+    // launches claim work from one 64-bit word — role 0 (clustered, cpt == 1) whole tiles
+    // from the bottom, role 1 (cluster-less) (tile, group) units from the top
+    unsigned long long* claim;
+    uint32_t role;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
@@ -178,6 +183,61 @@ __device__ __forceinline__ void kstep(double (&acc)[16][2], double (&sums)[4], d
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a * 4 + b][0], acc[a * 4 + b][1], r[a], r[4 + b]);
 }
 
+constexpr uint64_t kNoUnit = ~0ull;
+
+// The claim word: low 32 bits = tiles taken by role 0 from the bottom (a prefix [0, a)),
+// high 32 bits = units taken by role 1 from the top (tile T-1-b/G, group b%G).  Updated by
+// CAS only when the claim is valid, so a <= T - ceil(b/G) always holds: every tile is
+// processed once, wholly by one role.  Returns the unit (role 0: tile; role 1: tile*G+group).
+__device__ uint64_t claim_unit(unsigned long long* W, uint32_t role, uint64_t T, uint32_t G) {
+    unsigned long long old = atomicAdd(W, 0ull);
+    for (;;) {
+        const uint64_t a = old & 0xffffffffull, b = old >> 32;
+        unsigned long long nw;
+        uint64_t result;
+        if (role == 0) {
+            if (a + (b + G - 1) / G >= T) return kNoUnit;
+            nw = old + 1;
+            result = a;
+        } else {
+            const uint64_t tb = b / G;
+            if (tb >= T || T - 1 - tb < a) return kNoUnit;  // a started tile is always >= a
+            nw = old + (1ull << 32);
+            result = (T - 1 - tb) * G + b % G;
+        }
+        const unsigned long long seen = atomicCAS(W, old, nw);
+        if (seen == old) return result;
+        old = seen;
+    }
+}
+
+// Collective over the CTA (K = 1) or the cluster: one thread claims, everyone gets the unit.
+// Producer and consumer warps call it at the same unit boundaries from different code paths
+// (barrier.sync 1 / barrier.cluster count arrivals, not call sites).
+__device__ __forceinline__ uint64_t acquire_unit(const TileJob& job, const WideGeom& geo, uint32_t K, uint32_t it,
+                                                 uint64_t* s_claim) {
+    uint64_t* slot = &s_claim[it & 1];
+    const uint32_t rank = K > 1 ? cluster_rank() : 0;
+    if (threadIdx.x == 0 && rank == 0)
+        *slot = claim_unit(geo.claim, geo.role, job.tile_end - job.tile_begin, geo.n_groups);
+    if (K > 1) {
+        cluster_sync_all();
+        uint64_t v;
+        asm volatile(
+            "{\n"
+            ".reg .b32 ra;\n"
+            "mapa.shared::cluster.u32 ra, %1, 0;\n"
+            "ld.shared::cluster.u64 %0, [ra];\n"
+            "}\n"
+            : "=l"(v)
+            : "r"(smem_u32(slot))
+            : "memory");
+        return v;
+    }
+    asm volatile("barrier.sync 1;\n" ::: "memory");
+    return *(volatile uint64_t*)slot;
+}
+
 // One ring stage of SROWS rows: a straight-line program with the next k-step's fragment
 // loads issued under the current k-step's DMMAs.
 template <int SROWS, bool SUMS>
@@ -214,6 +274,23 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
     const uint32_t m = geo.cpt;
     const uint64_t units = (job.tile_end - job.tile_begin) * m;
     const uint64_t u_first = blockIdx.x / K, u_step = gridDim.x / K;
+    __shared__ uint64_t s_claim[2];
+    // unit -> (tile, group): static order (u / m, (u % m) K + rank), or claimed (role 0: the
+    // tile, group = rank; role 1: tile * n_groups + group)
+    auto next_unit = [&](uint64_t& u, uint32_t it) -> bool {
+        if (geo.claim) {
+            u = acquire_unit(job, geo, K, it, s_claim);
+            return u != kNoUnit;
+        }
+        if (it > 0) u += u_step;
+        return u < units;
+    };
+    auto unit_tile = [&](uint64_t u) -> uint64_t {
+        return job.tile_begin + (geo.claim ? (geo.role == 0 ? u : u / geo.n_groups) : u / m);
+    };
+    auto unit_group = [&](uint64_t u) -> uint32_t {
+        return geo.claim ? (geo.role == 0 ? rank : (uint32_t)(u % geo.n_groups)) : (uint32_t)(u % m) * K + rank;
+    };
 
     // the column pad [p, pitch) of every slot is never written by the copies: zero it once
     for (uint32_t i = threadIdx.x; i < ring * SROWS * (pitch - p); i += blockDim.x) {
@@ -234,8 +311,9 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
     if (warp == (int)consumers) {
         // ---------------- producer ----------------
         const uint16_t mask = (uint16_t)((1u << K) - 1);
-        for (uint64_t u = u_first; u < units; u += u_step) {
-            const UnitInfo ui = unit_info(job, geo, tile_rows, job.tile_begin + u / m);
+        uint64_t u = u_first;
+        for (uint32_t it = 0; next_unit(u, it); ++it) {
+            const UnitInfo ui = unit_info(job, geo, tile_rows, unit_tile(u));
             const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
             const double* crow = job.shift != nullptr ? job.shift + (uint64_t)ui.r * p : nullptr;
             for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
@@ -274,9 +352,10 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
         // ---------------- consumers ----------------
         const int g = lane >> 2, kk = lane & 3;
         const uint64_t E = partial_len(p);
-        for (uint64_t u = u_first; u < units; u += u_step) {
-            const UnitInfo ui = unit_info(job, geo, tile_rows, job.tile_begin + u / m);
-            const uint32_t grp = (uint32_t)(u % m) * K + rank;
+        uint64_t u = u_first;
+        for (uint32_t it = 0; next_unit(u, it); ++it) {
+            const UnitInfo ui = unit_info(job, geo, tile_rows, unit_tile(u));
+            const uint32_t grp = unit_group(u);
             const uint32_t item = __ldg(geo.items + grp * consumers + warp);
             const bool idle = item & kIdle;
             const uint32_t I = (item >> 14) & 0x3fff, J = item & 0x3fff;
@@ -361,19 +440,31 @@ struct Plan {
     uint32_t p = 0, srows = 0, grid_cap = 0;  // grid_cap = clusters in flight
     size_t smem = 0;
     WideGeom geo{};
+    uint32_t resident = 0;  // CTAs per SM the plan targets
+    // CTA slots the clustered plan leaves idle (cluster placement) run a cluster-less plan on
+    // a side stream over a proportional share of the tiles
+    bool has_spare = false;
+    uint32_t spare_ctas = 0;
+    size_t spare_smem = 0;
+    WideGeom spare_geo{};
 };
 std::mutex g_plan_mu;
+cudaStream_t g_side[64] = {};  // per-device side stream for the spare plan
 std::vector<Plan> g_plans;
 
 template <int SROWS>
-cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
+cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster = false) {
     auto kern = k_widep<SROWS>;
     const int threads = (int)(geo.consumers + 1) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     // the opt-in limit only caps what a launch may request; set it once to the maximum so
     // plans with different rings never invalidate each other
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    const size_t max_dyn = 227 * 1024 - fa.sharedSizeBytes;  // the claim slots are static
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn);
     if (e != cudaSuccess) return e;
     // deepest ring (2..4 stages) that keeps the target CTAs per SM (2 for 4-warp groups, so
     // two groups share an SM's four DMMA units; 1 for 8-warp groups)
@@ -383,7 +474,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
     for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", 4); ring >= 2; --ring) {
         geo.ring = ring;
         smem = sizeof(double) * ring * SROWS * geo.pitch + 2 * ring * sizeof(uint64_t);
-        if (smem > 227 * 1024) continue;
+        if (smem > max_dyn) continue;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
         if (e != cudaSuccess) return e;
         if (per_sm >= want) break;
@@ -398,7 +489,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
     const uint32_t items = geo.nr * (geo.nr + 1) / 2;
     const uint32_t groups = (items + geo.consumers - 1) / geo.consumers;
     const uint32_t kmax = std::min<uint32_t>(env_u32("SSTAT_WIDEP_MAXCLUSTER", 16), groups);
-    const bool nocluster = env_u32("SSTAT_WIDEP_NOCLUSTER", 0) != 0 || groups == 1;
+    const bool nocluster = force_nocluster || env_u32("SSTAT_WIDEP_NOCLUSTER", 0) != 0 || groups == 1;
     struct Cand {
         WideGeom g;
         int clusters;
@@ -458,6 +549,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out) {
     out.p = geo.p;
     out.srows = SROWS;
     out.grid_cap = best_clusters;
+    out.resident = (uint32_t)std::min(per_sm, want);
     out.smem = smem;
     out.geo = best;
     if (getenv("SSTAT_DEBUG"))
@@ -527,12 +619,63 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
                 : srows == 8 ? make_plan<8>(device, geo, pl)
                              : make_plan<4>(device, geo, pl);
             if (e != cudaSuccess) return e;
+            const uint64_t slots = (uint64_t)sms_of(device) * pl.resident;
+            const uint64_t used = (uint64_t)pl.grid_cap * pl.geo.csize;
+            // CTA slots the cluster placement leaves idle get a cluster-less launch (>= 4 % of
+            // the slots, whole-tile clusters only)
+            if (pl.geo.csize > 1 && pl.geo.cpt == 1 && slots > used && 25 * (slots - used) >= slots) {
+                Plan ps;
+                WideGeom g2 = geo;
+                g2.consumers = pl.geo.consumers;
+                e = srows == 16 ? make_plan<16>(device, g2, ps, true)
+                    : srows == 8 ? make_plan<8>(device, g2, ps, true)
+                                 : make_plan<4>(device, g2, ps, true);
+                if (e != cudaSuccess) return e;
+                if (!g_side[device]) {
+                    e = cudaStreamCreateWithFlags(&g_side[device], cudaStreamNonBlocking);
+                    if (e != cudaSuccess) return e;
+                }
+                pl.has_spare = true;
+                pl.spare_ctas = (uint32_t)(slots - used);
+                pl.spare_smem = ps.smem;
+                pl.spare_geo = ps.geo;
+            }
             if (!tuned) g_plans.push_back(pl);
         }
     }
-    return pl.srows == 16 ? launch_plan<16>(job, pl, stream)
-           : pl.srows == 8 ? launch_plan<8>(job, pl, stream)
-                           : launch_plan<4>(job, pl, stream);
+    if (!pl.has_spare || !job.claim || job.tile_end - job.tile_begin < 2 || env_u32("SSTAT_WIDEP_SPARE", 1) == 0)
+        return pl.srows == 16 ? launch_plan<16>(job, pl, stream)
+               : pl.srows == 8 ? launch_plan<8>(job, pl, stream)
+                               : launch_plan<4>(job, pl, stream);
+    // fork: the clustered plan on `stream` and the cluster-less plan on the side stream claim
+    // tiles / units dynamically from one word (claim_unit); if the side launch cannot run
+    // alongside, the clustered one simply takes every tile.  Join before returning.
+    unsigned long long* W = job.claim;  // the caller's scratch word (one launch at a time per caller)
+    if ((e = cudaMemsetAsync(W, 0, sizeof *W, stream)) != cudaSuccess) return e;
+    Plan pa = pl, pb = pl;
+    pa.geo.claim = W;
+    pa.geo.role = 0;
+    pb.geo = pl.spare_geo;
+    pb.geo.claim = W;
+    pb.geo.role = 1;
+    pb.grid_cap = pl.spare_ctas;
+    pb.smem = pl.spare_smem;
+    cudaStream_t side = g_side[device];
+    cudaEvent_t fork, join;
+    if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) != cudaSuccess) return e;
+    cudaEventRecord(fork, stream);
+    cudaStreamWaitEvent(side, fork, 0);
+    e = pl.srows == 16 ? launch_plan<16>(job, pa, stream) : pl.srows == 8 ? launch_plan<8>(job, pa, stream)
+                                                                          : launch_plan<4>(job, pa, stream);
+    cudaError_t e2 = pl.srows == 16 ? launch_plan<16>(job, pb, side)
+                     : pl.srows == 8 ? launch_plan<8>(job, pb, side)
+                                     : launch_plan<4>(job, pb, side);
+    cudaEventRecord(join, side);
+    cudaStreamWaitEvent(stream, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    return e != cudaSuccess ? e : e2;
 }
 
 }  // namespace sstat_b200

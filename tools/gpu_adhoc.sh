@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_next.py -q -m gpu -x 2>&1 | tail -3 > gpurun_out/pytest_new.log
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -4 > gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
