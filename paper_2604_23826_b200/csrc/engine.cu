@@ -629,7 +629,9 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             CUDA_TRY(c->d_claim.reserve(sizeof(unsigned long long)));
             j.claim = c->d_claim.as<unsigned long long>();
         }
-        CUDA_TRY(wide ? launch_widep(j, c->sms, s) : launch_smallp(j, c->sms, s));
+        uint32_t kernels = 1;
+        CUDA_TRY(wide ? launch_widep(j, c->sms, s, &kernels) : launch_smallp(j, c->sms, s));
+        if (tm) tm->kernel_launches += kernels - 1;  // the callers count one accumulate kernel
     };
 
     CUDA_TRY(cudaEventRecord(c->ev[0], s));

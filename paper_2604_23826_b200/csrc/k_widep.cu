@@ -585,7 +585,8 @@ cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream)
 
 uint32_t widep_tile_rows(uint32_t) { return 32768; }
 
-cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
+cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t* kernels) {
+    if (kernels) *kernels = 1;
     const uint32_t p = job.p;
     if (p > kMaxWideP || p < 2) return cudaErrorInvalidValue;
     int device = 0;
@@ -673,6 +674,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream) {
                                      : launch_plan<4>(job, pb, side);
     cudaEventRecord(join, side);
     cudaStreamWaitEvent(stream, join, 0);
+    if (kernels) *kernels = 2;
     cudaEventDestroy(fork);
     cudaEventDestroy(join);
     return e != cudaSuccess ? e : e2;

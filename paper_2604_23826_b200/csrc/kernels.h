@@ -13,7 +13,8 @@ namespace sstat_b200 {
 cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream);
 
 // K2: tiles for p > 64 (smem-staged DMMA SYRK), tiles of widep_tile_rows(p) rows.
-cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream);
+// *kernels (optional) receives the number of kernels launched (2 when the idle-slot split runs).
+cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream, uint32_t* kernels = nullptr);
 uint32_t widep_tile_rows(uint32_t p);
 constexpr uint32_t kMaxWideP = 2048;  // launch_widep rejects wider rows
 

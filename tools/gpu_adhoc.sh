@@ -1,2 +1,2 @@
-timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -4 > gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 5 --warmup 3 --config c5 > gpurun_out/bench_c5.log 2>&1
+timeout 600 python -m pytest tests -q -m gpu -x -k "wide_p_schedule or c5 or comoments_wide" 2>&1 | tail -2 > gpurun_out/pytest_new.log
