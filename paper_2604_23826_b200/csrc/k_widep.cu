@@ -25,7 +25,14 @@
 //     the slot's `empty` mbarrier of every CTA of the cluster (mapa + remote arrive).
 // Column sums of rectangle J ride on the warp that owns rectangle (0, J).  Each (tile, group)
 // writes disjoint entries of the tile's canonical partial, so the result is a fixed
-// function of the tile (independent of C, clusters, grid and ring depth).
+// function of the tile (independent of C, clusters, grid, ring depth and work split).
+//
+// Launch geometry is chosen once per (device, p) from the occupancy calculator (make_plan).
+// When cluster placement leaves CTA slots idle, a second, cluster-less launch fills them on a
+// side stream and both claim work dynamically from one CAS-updated word (claim_unit).
+// SSTAT_WIDEP_* environment variables override the choices for experiments and tests:
+// CONSUMERS (4 | 8), CLUSTER / MAXCLUSTER (K), NOCLUSTER, RING, SROWS (8 for p <= 256),
+// PERSM (CTAs per SM), SPARE=0 (no side launch), DEBUG (print the plan).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
