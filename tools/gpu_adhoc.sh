@@ -1,1 +1,1 @@
-start=$(date +%s); timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo "took $(( $(date +%s) - start )) s" >> gpurun_out/bench_default.log
+timeout 900 python tools/p_sweep.py > gpurun_out/p_sweep.log 2>&1
