@@ -1,1 +1,1 @@
-timeout 900 python tools/p_sweep.py > gpurun_out/p_sweep.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
