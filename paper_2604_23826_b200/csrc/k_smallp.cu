@@ -17,6 +17,7 @@
 // NB contiguous doubles with 128-bit loads;  otherwise J*8 + g — 8 lanes read 8
 // consecutive doubles of a row per instruction (64-byte segments).
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -96,10 +97,8 @@ __device__ int canonical_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-// No occupancy floor: unbounded, NB <= 2 compiles to 64 registers (4 CTAs, 32 warps per SM)
-// and NB <= 4 to ~85 (3 CTAs); a cap only forces spills.
 template <int NB, bool VEC>
-__global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
+__device__ __forceinline__ void smallp_body(const TileJob& job) {
     using C = SmallP<NB, VEC>;
     constexpr int U = C::U;
     extern __shared__ double red[];  // [kWarps][FRAG]
@@ -190,26 +189,56 @@ __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
     }
 }
 
+// The same body under different register budgets.  Unbounded: NB <= 2 compiles to 64
+// registers (4 CTAs, 32 warps per SM) and a floor there only changes the allocation for the
+// worse.  The wider widths are load-latency-bound at the occupancy their unbounded register
+// counts allow, so they take a floor of MINB CTAs per SM (measured per NB, SSTAT_K1_MINB
+// overrides): 3 for NB = 3..4 (<= 85 registers, 24 warps; p = 24: 4.2 -> 5.8 TB/s, p = 32:
+// 4.2 -> 5.0), 2 for NB = 5 (<= 128; p = 40: +35 %).  NB = 6 spills under a floor of 2 and
+// loses 14 %; NB >= 6 stay unbounded.
+template <int NB, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
+    smallp_body<NB, VEC>(job);
+}
+template <int NB, bool VEC, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_smallp_floor(TileJob job) {
+    smallp_body<NB, VEC>(job);
+}
+
 template <int NB, bool VEC>
 cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, VEC>::FRAG;
-    // function attribute + occupancy, once per device (kept off the per-call path)
-    static std::atomic<int> cached[64];
+    int minb = NB == 3 || NB == 4 ? 3 : (NB == 5 ? 2 : 0);
+    if (const char* env = getenv("SSTAT_K1_MINB")) minb = atoi(env);
+    void (*kern)(TileJob) = k_smallp<NB, VEC>;
+    if constexpr (NB >= 3 && NB <= 4) {
+        if (minb == 3) kern = k_smallp_floor<NB, VEC, 3>;
+        else if (minb == 2) kern = k_smallp_floor<NB, VEC, 2>;
+        else minb = 0;
+    } else if constexpr (NB == 5) {
+        if (minb == 2) kern = k_smallp_floor<NB, VEC, 2>;
+        else minb = 0;
+    } else {
+        minb = 0;
+    }
+    const int variant = minb;  // 0, 2 or 3
+    // function attribute + occupancy, once per device and variant (kept off the per-call path)
+    static std::atomic<int> cached[4][64];
     int dev = 0;
     cudaGetDevice(&dev);
-    int per_sm = dev < 64 ? cached[dev].load() : 0;
+    int per_sm = dev < 64 ? cached[variant][dev].load() : 0;
     if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_smallp<NB, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp<NB, VEC>, kThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
-        if (dev < 64) cached[dev].store(per_sm);
+        if (dev < 64) cached[variant][dev].store(per_sm);
     }
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
-    k_smallp<NB, VEC><<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    kern<<<(unsigned)grid, kThreads, smem, stream>>>(job);
     return cudaGetLastError();
 }
 
