@@ -176,20 +176,20 @@ __device__ __forceinline__ void load_frags(double (&r)[8], const double* st, int
 // DADD shares the FP64 pipe with DMMA (profiles/r01_fp64_mix_probe.log): only the warps that
 // own a rectangle (0, J) add the column sums (SUMS), the others issue 8 DADD per 16 DMMA.
 template <bool SUMS>
-__device__ __forceinline__ void kstep(double (&acc)[16][2], double (&sums)[4], double (&r)[8],
-                                      const double (&cw)[8]) {
+__device__ __forceinline__ void kprep(double (&sums)[4], double (&r)[8], const double (&cw)[8]) {
 #pragma unroll
     for (int a = 0; a < 8; ++a) r[a] -= cw[a];
     if (SUMS) {
 #pragma unroll
         for (int a = 0; a < 4; ++a) sums[a] += r[4 + a];
     }
+}
+__device__ __forceinline__ void kmma(double (&acc)[16][2], const double (&r)[8]) {
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a * 4 + b][0], acc[a * 4 + b][1], r[a], r[4 + b]);
 }
-
 constexpr uint64_t kNoUnit = ~0ull;
 
 // The claim word: low 32 bits = tiles taken by role 0 from the bottom (a prefix [0, a)),
@@ -246,18 +246,28 @@ __device__ __forceinline__ uint64_t acquire_unit(const TileJob& job, const WideG
 }
 
 // One ring stage of SROWS rows: a straight-line program with the next k-step's fragment
-// loads issued under the current k-step's DMMAs.
-template <int SROWS, bool SUMS>
+// loads issued under the current k-step's DMMAs.  The slot is released (release()) as soon as
+// the last k-step's fragments have been consumed by its shift subtraction — before that
+// k-step's DMMAs — so the producers can refill it a k-step earlier.
+template <int SROWS, bool SUMS, class Release>
 __device__ __forceinline__ void consume_stage(double (&acc)[16][2], double (&sums)[4], const double* st,
-                                              uint32_t pitch, int colI, int colJ, const double (&cw)[8]) {
+                                              uint32_t pitch, int colI, int colJ, const double (&cw)[8],
+                                              Release&& release) {
+    constexpr int Q = SROWS / 4;
     double ra[8], rb[8];
     load_frags(ra, st, colI, colJ);
 #pragma unroll
-    for (int q = 0; q < SROWS / 4; q += 2) {
-        if (q + 1 < SROWS / 4) load_frags(rb, st + 4 * (q + 1) * pitch, colI, colJ);
-        kstep<SUMS>(acc, sums, ra, cw);
-        if (q + 2 < SROWS / 4) load_frags(ra, st + 4 * (q + 2) * pitch, colI, colJ);
-        if (q + 1 < SROWS / 4) kstep<SUMS>(acc, sums, rb, cw);
+    for (int q = 0; q < Q; q += 2) {
+        if (q + 1 < Q) load_frags(rb, st + 4 * (q + 1) * pitch, colI, colJ);
+        kprep<SUMS>(sums, ra, cw);
+        if (q + 1 == Q) release();
+        kmma(acc, ra);
+        if (q + 2 < Q) load_frags(ra, st + 4 * (q + 2) * pitch, colI, colJ);
+        if (q + 1 < Q) {
+            kprep<SUMS>(sums, rb, cw);
+            if (q + 2 == Q) release();
+            kmma(acc, rb);
+        }
     }
 }
 
@@ -387,12 +397,16 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
                 mbar_wait(&full[slot], ph);
                 // an idle (padding) warp of the last group keeps the ring protocol only
                 const double* st = sm + slot * slot_elems + kk * pitch;
+                auto release = [&]() {
+                    __syncwarp();
+                    if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[slot], lane);
+                };
                 if (sums_here)
-                    consume_stage<SROWS, true>(acc, sums, st, pitch, colI, colJ, cw);
+                    consume_stage<SROWS, true>(acc, sums, st, pitch, colI, colJ, cw, release);
                 else if (!idle)
-                    consume_stage<SROWS, false>(acc, sums, st, pitch, colI, colJ, cw);
-                __syncwarp();
-                if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[slot], lane);
+                    consume_stage<SROWS, false>(acc, sums, st, pitch, colI, colJ, cw, release);
+                else
+                    release();
                 if (++slot == ring) slot = 0, ph ^= 1;
             }
 
