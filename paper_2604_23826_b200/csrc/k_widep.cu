@@ -52,6 +52,10 @@ int sms_of(int device) {
 }
 
 constexpr uint32_t kIdle = 1u << 28;
+// Fragment reads of the padded rectangle columns (up to 32 nr - 1 >= p) run past a row's
+// pitch into the next row (harmless: those blocks are dropped) and, on a slot's last row,
+// past the ring: kSlack doubles of shared memory keep them inside the allocation.
+constexpr uint32_t kSlack = 32;
 
 struct WideGeom {
     uint32_t p, nb, nr, pitch, n_groups, consumers, ring;
@@ -73,6 +77,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 // arrive on the barrier at the same smem offset in cluster CTA `cta`
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
@@ -124,9 +131,6 @@ __device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;\n" ::: "memory");
@@ -276,14 +280,20 @@ __device__ __forceinline__ void consume_stage(double (&acc)[16][2], double (&sum
 // cluster dimension geo.csize (1 = no cluster).
 template <int SROWS>
 __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t tile_rows) {
-    extern __shared__ __align__(128) double sm[];  // ring x (SROWS x pitch) | full[ring] | empty[ring]
+    // ring x (SROWS x pitch) | kSlack doubles | full[ring] | empty[ring]
+    extern __shared__ __align__(128) double sm[];
     const uint32_t p = geo.p, pitch = geo.pitch, nb = geo.nb, ring = geo.ring, K = geo.csize;
     const uint32_t slot_elems = SROWS * pitch;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ring * slot_elems);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ring * slot_elems + kSlack);
     uint64_t* empty = full + ring;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t consumers = geo.consumers;
-    const bool bulk = (p % 2 == 0) && (reinterpret_cast<uintptr_t>(job.base) % 16 == 0);
+    // even p: one TMA bulk copy per row (rows 16-byte aligned when the base is); odd p: rows
+    // are 8 (mod 16) bytes long, so row PAIRS are copied (pitch = p, unpadded) and an odd last
+    // row goes as p - 1 doubles + 1 plain store; otherwise (base not 16-byte aligned, or an
+    // odd p stage starting on an odd row) 8-byte cp.async from all lanes, waited on by the
+    // producer itself.  `full` always expects one arrival (the producer's lane 0).
+    const bool even_p = (p % 2 == 0);
     // unit u = (tile u / m, cluster part u % m) covers groups [(u % m) K, (u % m + 1) K) of
     // the tile; cluster c (K consecutive CTAs) runs units c, c + n_clusters, ... so the m
     // parts of a tile start side by side
@@ -316,7 +326,7 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
     }
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < ring; ++s) {
-            mbar_init(&full[s], bulk ? 1u : 32u);
+            mbar_init(&full[s], 1u);
             mbar_init(&empty[s], consumers * K);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -344,8 +354,11 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
                 // stores, ordered before the release of this lane's arrive below)
                 for (uint32_t rr = vrows; rr < SROWS; ++rr)
                     for (uint32_t j = lane; j < p; j += 32) dst[rr * pitch + j] = crow ? crow[j] : 0.0;
+                const bool aligned = (reinterpret_cast<uintptr_t>(src) % 16) == 0;
+                if (!even_p && aligned && (vrows & 1) && lane == 0)  // odd last row: its last double
+                    dst[(vrows - 1) * pitch + p - 1] = src[(uint64_t)(vrows - 1) * p + p - 1];
                 __syncwarp();
-                if (bulk) {
+                if (aligned && even_p) {
                     if (lane == 0) {
                         // this CTA receives every valid row of the stage, from all K producers
                         mbar_arrive_expect_tx(&full[slot], vrows * p * 8);
@@ -357,10 +370,31 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
                                 bulk_g2s(dst + rr * pitch, src + (uint64_t)rr * p, p * 8, &full[slot]);
                         }
                     }
+                } else if (aligned) {  // odd p, pitch == p: pairs of rows are 16-byte multiples
+                    if (lane == 0) {
+                        const uint32_t npairs = vrows / 2;
+                        const bool odd_last = vrows & 1;
+                        mbar_arrive_expect_tx(&full[slot], npairs * 16 * p + (odd_last ? 8 * (p - 1) : 0));
+                        for (uint32_t i = rank; i < npairs; i += K) {
+                            if (K > 1)
+                                bulk_g2s_mc(dst + 2 * i * pitch, src + (uint64_t)2 * i * p, p * 16, &full[slot], mask);
+                            else
+                                bulk_g2s(dst + 2 * i * pitch, src + (uint64_t)2 * i * p, p * 16, &full[slot]);
+                        }
+                        if (odd_last && npairs % K == rank) {
+                            double* d = dst + (vrows - 1) * pitch;
+                            const double* g = src + (uint64_t)(vrows - 1) * p;
+                            if (K > 1) bulk_g2s_mc(d, g, (p - 1) * 8, &full[slot], mask);
+                            else bulk_g2s(d, g, (p - 1) * 8, &full[slot]);
+                        }
+                    }
                 } else {
+                    // every CTA stages its own copy (no multicast), then arrives once complete
                     for (uint32_t rr = 0; rr < vrows; ++rr)
                         for (uint32_t j = lane; j < p; j += 32) cp_async8(dst + rr * pitch + j, src + (uint64_t)rr * p + j);
-                    cp_async_arrive_noinc(&full[slot]);
+                    asm volatile("cp.async.wait_all;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_local(&full[slot]);
                 }
                 if (++slot == ring) slot = 0, ph ^= 1;
             }
@@ -494,7 +528,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster 
     int per_sm = 0;
     for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", 4); ring >= 2; --ring) {
         geo.ring = ring;
-        smem = sizeof(double) * ring * SROWS * geo.pitch + 2 * ring * sizeof(uint64_t);
+        smem = sizeof(double) * (ring * SROWS * geo.pitch + kSlack) + 2 * ring * sizeof(uint64_t);
         if (smem > max_dyn) continue;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
         if (e != cudaSuccess) return e;
@@ -632,7 +666,8 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
             geo.nr = (geo.nb + 3) / 4;
             // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank
             // groups, so each half-warp fragment read is one conflict-free wavefront
-            geo.pitch = ((p + 15) / 16) * 16 + 4;
+            // (odd p: unpadded, the stage is copied as row pairs; see k_widep)
+            geo.pitch = p % 2 ? p : ((p + 15) / 16) * 16 + 4;
             // 4-warp groups (two CTAs per SM) leave at most 3 idle rectangles per tile, 8-warp
             // groups up to 7 but re-read less; the multicast makes the extra groups cheap
             const uint32_t items = geo.nr * (geo.nr + 1) / 2;
