@@ -59,6 +59,7 @@ constexpr uint32_t kSlack = 32;
 
 struct WideGeom {
     uint32_t p, nb, nr, pitch, n_groups, consumers, ring;
+    uint32_t R;              // rectangle side in 8-column blocks (nr = ceil(nb / R))
     uint32_t csize;          // CTAs per cluster (K)
     uint32_t cpt;            // clusters per tile (m); n_groups == K * m
     const uint32_t* items;   // device [n_groups][consumers]: idle<<28 | I<<14 | J
@@ -172,28 +173,31 @@ __device__ __forceinline__ UnitInfo unit_info(const TileJob& job, const WideGeom
     return ui;
 }
 
-// One k-step: 4 rows of the stage at `st` (lane kk reads row kk) for the 8 fragments.
-__device__ __forceinline__ void load_frags(double (&r)[8], const double* st, int colI, int colJ) {
+// One k-step: 4 rows of the stage at `st` (lane kk reads row kk) for the 2R fragments.
+template <int R>
+__device__ __forceinline__ void load_frags(double (&r)[2 * R], const double* st, int colI, int colJ) {
 #pragma unroll
-    for (int a = 0; a < 8; ++a) r[a] = st[a < 4 ? colI + 8 * a : colJ + 8 * (a - 4)];
+    for (int a = 0; a < 2 * R; ++a) r[a] = st[a < R ? colI + 8 * a : colJ + 8 * (a - R)];
 }
 // DADD shares the FP64 pipe with DMMA (profiles/r01_fp64_mix_probe.log): only the warps that
-// own a rectangle (0, J) add the column sums (SUMS), the others issue 8 DADD per 16 DMMA.
-template <bool SUMS>
-__device__ __forceinline__ void kprep(double (&sums)[4], double (&r)[8], const double (&cw)[8]) {
+// own a rectangle (0, J) add the column sums (SUMS), the others issue 2R DADD per R*R DMMA.
+template <bool SUMS, int R>
+__device__ __forceinline__ void kprep(double (&sums)[R], double (&r)[2 * R], const double (&cw)[2 * R]) {
 #pragma unroll
-    for (int a = 0; a < 8; ++a) r[a] -= cw[a];
+    for (int a = 0; a < 2 * R; ++a) r[a] -= cw[a];
     if (SUMS) {
 #pragma unroll
-        for (int a = 0; a < 4; ++a) sums[a] += r[4 + a];
+        for (int a = 0; a < R; ++a) sums[a] += r[R + a];
     }
 }
-__device__ __forceinline__ void kmma(double (&acc)[16][2], const double (&r)[8]) {
+template <int R>
+__device__ __forceinline__ void kmma(double (&acc)[R * R][2], const double (&r)[2 * R]) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a * 4 + b][0], acc[a * 4 + b][1], r[a], r[4 + b]);
+        for (int b = 0; b < R; ++b) dmma_8x8x4(acc[a * R + b][0], acc[a * R + b][1], r[a], r[R + b]);
 }
+
 constexpr uint64_t kNoUnit = ~0ull;
 
 // The claim word: low 32 bits = tiles taken by role 0 from the bottom (a prefix [0, a)),
@@ -253,24 +257,24 @@ __device__ __forceinline__ uint64_t acquire_unit(const TileJob& job, const WideG
 // loads issued under the current k-step's DMMAs.  The slot is released (release()) as soon as
 // the last k-step's fragments have been consumed by its shift subtraction — before that
 // k-step's DMMAs — so the producers can refill it a k-step earlier.
-template <int SROWS, bool SUMS, class Release>
-__device__ __forceinline__ void consume_stage(double (&acc)[16][2], double (&sums)[4], const double* st,
-                                              uint32_t pitch, int colI, int colJ, const double (&cw)[8],
+template <int SROWS, int R, bool SUMS, class Release>
+__device__ __forceinline__ void consume_stage(double (&acc)[R * R][2], double (&sums)[R], const double* st,
+                                              uint32_t pitch, int colI, int colJ, const double (&cw)[2 * R],
                                               Release&& release) {
     constexpr int Q = SROWS / 4;
-    double ra[8], rb[8];
-    load_frags(ra, st, colI, colJ);
+    double ra[2 * R], rb[2 * R];
+    load_frags<R>(ra, st, colI, colJ);
 #pragma unroll
     for (int q = 0; q < Q; q += 2) {
-        if (q + 1 < Q) load_frags(rb, st + 4 * (q + 1) * pitch, colI, colJ);
-        kprep<SUMS>(sums, ra, cw);
+        if (q + 1 < Q) load_frags<R>(rb, st + 4 * (q + 1) * pitch, colI, colJ);
+        kprep<SUMS, R>(sums, ra, cw);
         if (q + 1 == Q) release();
-        kmma(acc, ra);
-        if (q + 2 < Q) load_frags(ra, st + 4 * (q + 2) * pitch, colI, colJ);
+        kmma<R>(acc, ra);
+        if (q + 2 < Q) load_frags<R>(ra, st + 4 * (q + 2) * pitch, colI, colJ);
         if (q + 1 < Q) {
-            kprep<SUMS>(sums, rb, cw);
+            kprep<SUMS, R>(sums, rb, cw);
             if (q + 2 == Q) release();
-            kmma(acc, rb);
+            kmma<R>(acc, rb);
         }
     }
 }
@@ -278,7 +282,7 @@ __device__ __forceinline__ void consume_stage(double (&acc)[16][2], double (&sum
 // SROWS = rows per ring stage (compile-time, so a stage is one straight-line program with
 // the next k-step's fragment loads issued under the current k-step's DMMAs).  Launched with
 // cluster dimension geo.csize (1 = no cluster).
-template <int SROWS>
+template <int SROWS, int R>
 __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t tile_rows) {
     // ring x (SROWS x pitch) | kSlack doubles | full[ring] | empty[ring]
     extern __shared__ __align__(128) double sm[];
@@ -410,21 +414,21 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
             const uint32_t item = __ldg(geo.items + grp * consumers + warp);
             const bool idle = item & kIdle;
             const uint32_t I = (item >> 14) & 0x3fff, J = item & 0x3fff;
-            // fragment a reads column colI + 8a (a < 4, rectangle I) or colJ + 8(a-4) (rectangle
+            // fragment a reads column colI + 8a (a < R, rectangle I) or colJ + 8(a-R) (rectangle
             // J); columns past p read the zero pad with c = 0, rows past the tile end read c
-            const int colI = (int)(32 * I) + g, colJ = (int)(32 * J) + g;
+            const int colI = (int)(8 * R * I) + g, colJ = (int)(8 * R * J) + g;
             const bool sums_here = !idle && I == 0;  // rectangle (0, J) sums rectangle J's columns
-            double cw[8];
+            double cw[2 * R];
 #pragma unroll
-            for (int a = 0; a < 8; ++a) {
-                const int col = a < 4 ? colI + 8 * a : colJ + 8 * (a - 4);
+            for (int a = 0; a < 2 * R; ++a) {
+                const int col = a < R ? colI + 8 * a : colJ + 8 * (a - R);
                 cw[a] = (!idle && col < (int)p && job.shift != nullptr) ? job.shift[(uint64_t)ui.r * p + col] : 0.0;
             }
-            double acc[16][2], sums[4];
+            double acc[R * R][2], sums[R];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+            for (int i = 0; i < R * R; ++i) acc[i][0] = acc[i][1] = 0.0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) sums[i] = 0.0;
+            for (int i = 0; i < R; ++i) sums[i] = 0.0;
 
             const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
             for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
@@ -436,9 +440,9 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
                     if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[slot], lane);
                 };
                 if (sums_here)
-                    consume_stage<SROWS, true>(acc, sums, st, pitch, colI, colJ, cw, release);
+                    consume_stage<SROWS, R, true>(acc, sums, st, pitch, colI, colJ, cw, release);
                 else if (!idle)
-                    consume_stage<SROWS, false>(acc, sums, st, pitch, colI, colJ, cw, release);
+                    consume_stage<SROWS, R, false>(acc, sums, st, pitch, colI, colJ, cw, release);
                 else
                     release();
                 if (++slot == ring) slot = 0, ph ^= 1;
@@ -448,22 +452,22 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
             double* out = job.tile_partials + ui.t * E;
             if (!idle) {
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                for (int a = 0; a < R; ++a)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const uint32_t A = 4 * I + a, B = 4 * J + b;
-                        if (A <= B && B < nb) write_block(out, p, A, B, g, kk, acc[a * 4 + b]);
+                    for (int b = 0; b < R; ++b) {
+                        const uint32_t A = R * I + a, B = R * J + b;
+                        if (A <= B && B < nb) write_block(out, p, A, B, g, kk, acc[a * R + b]);
                     }
             }
             if (sums_here) {
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
+                for (int a = 0; a < R; ++a) {
                     sums[a] += __shfl_xor_sync(0xffffffffu, sums[a], 1);
                     sums[a] += __shfl_xor_sync(0xffffffffu, sums[a], 2);
                 }
                 if (kk == 0) {
 #pragma unroll
-                    for (int a = 0; a < 4; ++a)
+                    for (int a = 0; a < R; ++a)
                         if (colJ + 8 * a < (int)p) out[colJ + 8 * a] = sums[a];
                 }
             }
@@ -492,7 +496,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // rectangle table kept on the device for the life of the process.
 struct Plan {
     int device = -1;
-    uint32_t p = 0, srows = 0, grid_cap = 0;  // grid_cap = clusters in flight
+    uint32_t p = 0, srows = 0, R = 0, grid_cap = 0;  // grid_cap = clusters in flight
     size_t smem = 0;
     WideGeom geo{};
     uint32_t resident = 0;  // CTAs per SM the plan targets
@@ -507,9 +511,9 @@ std::mutex g_plan_mu;
 cudaStream_t g_side[64] = {};  // per-device side stream for the spare plan
 std::vector<Plan> g_plans;
 
-template <int SROWS>
+template <int SROWS, int R>
 cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster = false) {
-    auto kern = k_widep<SROWS>;
+    auto kern = k_widep<SROWS, R>;
     const int threads = (int)(geo.consumers + 1) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
@@ -523,7 +527,8 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster 
     if (e != cudaSuccess) return e;
     // deepest ring (2..4 stages) that keeps the target CTAs per SM (2 for 4-warp groups, so
     // two groups share an SM's four DMMA units; 1 for 8-warp groups)
-    const int want = (int)env_u32("SSTAT_WIDEP_PERSM", geo.consumers == 4 ? 2 : 1);
+    // smaller rectangles need fewer registers: three 4-warp CTAs per SM
+    const int want = (int)env_u32("SSTAT_WIDEP_PERSM", geo.consumers == 4 ? (R == 4 ? 2 : 3) : 1);
     size_t smem = 0;
     int per_sm = 0;
     for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", 4); ring >= 2; --ring) {
@@ -603,18 +608,19 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster 
     out.device = device;
     out.p = geo.p;
     out.srows = SROWS;
+    out.R = R;
     out.grid_cap = best_clusters;
     out.resident = (uint32_t)std::min(per_sm, want);
     out.smem = smem;
     out.geo = best;
     if (getenv("SSTAT_DEBUG"))
-        fprintf(stderr, "k_widep<%d>: p=%u C=%u groups=%u/%u cluster=%u x %u ring=%u smem=%zu per_sm=%d clusters=%u\n",
-                SROWS, geo.p, best.consumers, groups, best.n_groups, best.csize, best.cpt, best.ring, smem, per_sm,
+        fprintf(stderr, "k_widep<%d,%d>: p=%u C=%u groups=%u/%u cluster=%u x %u ring=%u smem=%zu per_sm=%d clusters=%u\n",
+                SROWS, R, geo.p, best.consumers, groups, best.n_groups, best.csize, best.cpt, best.ring, smem, per_sm,
                 best_clusters);
     return cudaSuccess;
 }
 
-template <int SROWS>
+template <int SROWS, int R>
 cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream) {
     const uint64_t tiles = job.tile_end - job.tile_begin;
     if (tiles == 0) return cudaSuccess;
@@ -631,9 +637,47 @@ cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream)
     cfg.numAttrs = 1;
     const uint64_t units = tiles * pl.geo.cpt;
     cfg.gridDim = dim3((unsigned)(std::min<uint64_t>(units, pl.grid_cap) * pl.geo.csize));
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_widep<SROWS>, job, pl.geo, widep_tile_rows(pl.geo.p));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_widep<SROWS, R>, job, pl.geo, widep_tile_rows(pl.geo.p));
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+template <int SROWS>
+cudaError_t make_plan_r(int device, const WideGeom& geo, Plan& out, bool force_nocluster) {
+    return geo.R == 2 ? make_plan<SROWS, 2>(device, geo, out, force_nocluster)
+           : geo.R == 3 ? make_plan<SROWS, 3>(device, geo, out, force_nocluster)
+                        : make_plan<SROWS, 4>(device, geo, out, force_nocluster);
+}
+cudaError_t make_plan_any(int device, const WideGeom& geo, uint32_t srows, Plan& out, bool force_nocluster = false) {
+    return srows == 16 ? make_plan_r<16>(device, geo, out, force_nocluster)
+           : srows == 8 ? make_plan_r<8>(device, geo, out, force_nocluster)
+                        : make_plan_r<4>(device, geo, out, force_nocluster);
+}
+template <int SROWS>
+cudaError_t launch_plan_r(const TileJob& job, const Plan& pl, cudaStream_t stream) {
+    return pl.R == 2 ? launch_plan<SROWS, 2>(job, pl, stream)
+           : pl.R == 3 ? launch_plan<SROWS, 3>(job, pl, stream)
+                       : launch_plan<SROWS, 4>(job, pl, stream);
+}
+cudaError_t launch_plan_any(const TileJob& job, const Plan& pl, cudaStream_t stream) {
+    return pl.srows == 16 ? launch_plan_r<16>(job, pl, stream)
+           : pl.srows == 8 ? launch_plan_r<8>(job, pl, stream)
+                           : launch_plan_r<4>(job, pl, stream);
+}
+
+// Rectangle side R (8-column blocks): the fewest DMMA-equivalents per useful block over the
+// warp slots of a tile (idle padding included), R*R DMMA + R/4 for the 2R shift DADDs per
+// warp k-step; ties go to the larger R (fewer groups re-reading the tile).
+uint32_t choose_r(uint32_t nb, uint32_t consumers) {
+    uint32_t best = 4;
+    double best_cost = 0;
+    for (uint32_t R : {4u, 3u, 2u}) {
+        const uint32_t nr = (nb + R - 1) / R, items = nr * (nr + 1) / 2;
+        const uint32_t slots = (items + consumers - 1) / consumers * consumers;
+        const double cost = slots * (R * R + R / 4.0) / (nb * (nb + 1) / 2.0);
+        if (best_cost == 0 || cost < 0.97 * best_cost) best = R, best_cost = cost;
+    }
+    return best;
 }
 
 }  // namespace
@@ -651,7 +695,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
     uint32_t srows = p <= 256 ? 16 : p <= 512 ? 8 : 4;
     if (p <= 256 && env_u32("SSTAT_WIDEP_SROWS", 16) == 8) srows = 8;
     const bool tuned = getenv("SSTAT_WIDEP_CONSUMERS") || getenv("SSTAT_WIDEP_NOCLUSTER") ||
-                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS") || getenv("SSTAT_WIDEP_PERSM");
+                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS") || getenv("SSTAT_WIDEP_PERSM") || getenv("SSTAT_WIDEP_R");
     Plan pl;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -663,7 +707,9 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
             WideGeom geo{};
             geo.p = p;
             geo.nb = (p + 7) / 8;
-            geo.nr = (geo.nb + 3) / 4;
+            geo.R = env_u32("SSTAT_WIDEP_R", choose_r(geo.nb, 4));
+            if (geo.R < 2 || geo.R > 4) geo.R = 4;
+            geo.nr = (geo.nb + geo.R - 1) / geo.R;
             // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank
             // groups, so each half-warp fragment read is one conflict-free wavefront
             // (odd p: unpadded, the stage is copied as row pairs; see k_widep)
@@ -672,9 +718,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
             // groups up to 7 but re-read less; the multicast makes the extra groups cheap
             const uint32_t items = geo.nr * (geo.nr + 1) / 2;
             geo.consumers = env_u32("SSTAT_WIDEP_CONSUMERS", items <= 64 ? 4 : 8) == 4 ? 4 : 8;
-            e = srows == 16 ? make_plan<16>(device, geo, pl)
-                : srows == 8 ? make_plan<8>(device, geo, pl)
-                             : make_plan<4>(device, geo, pl);
+            e = make_plan_any(device, geo, srows, pl);
             if (e != cudaSuccess) return e;
             const uint64_t slots = (uint64_t)sms_of(device) * pl.resident;
             const uint64_t used = (uint64_t)pl.grid_cap * pl.geo.csize;
@@ -684,9 +728,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
                 Plan ps;
                 WideGeom g2 = geo;
                 g2.consumers = pl.geo.consumers;
-                e = srows == 16 ? make_plan<16>(device, g2, ps, true)
-                    : srows == 8 ? make_plan<8>(device, g2, ps, true)
-                                 : make_plan<4>(device, g2, ps, true);
+                e = make_plan_any(device, g2, srows, ps, true);
                 if (e != cudaSuccess) return e;
                 if (!g_side[device]) {
                     e = cudaStreamCreateWithFlags(&g_side[device], cudaStreamNonBlocking);
@@ -701,9 +743,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
         }
     }
     if (!pl.has_spare || !job.claim || job.tile_end - job.tile_begin < 2 || env_u32("SSTAT_WIDEP_SPARE", 1) == 0)
-        return pl.srows == 16 ? launch_plan<16>(job, pl, stream)
-               : pl.srows == 8 ? launch_plan<8>(job, pl, stream)
-                               : launch_plan<4>(job, pl, stream);
+        return launch_plan_any(job, pl, stream);
     // fork: the clustered plan on `stream` and the cluster-less plan on the side stream claim
     // tiles / units dynamically from one word (claim_unit); if the side launch cannot run
     // alongside, the clustered one simply takes every tile.  Join before returning.
@@ -723,11 +763,8 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
     if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) != cudaSuccess) return e;
     cudaEventRecord(fork, stream);
     cudaStreamWaitEvent(side, fork, 0);
-    e = pl.srows == 16 ? launch_plan<16>(job, pa, stream) : pl.srows == 8 ? launch_plan<8>(job, pa, stream)
-                                                                          : launch_plan<4>(job, pa, stream);
-    cudaError_t e2 = pl.srows == 16 ? launch_plan<16>(job, pb, side)
-                     : pl.srows == 8 ? launch_plan<8>(job, pb, side)
-                                     : launch_plan<4>(job, pb, side);
+    e = launch_plan_any(job, pa, stream);
+    cudaError_t e2 = launch_plan_any(job, pb, side);
     cudaEventRecord(join, side);
     cudaStreamWaitEvent(stream, join, 0);
     if (kernels) *kernels = 2;

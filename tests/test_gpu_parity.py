@@ -531,7 +531,7 @@ def test_widest_fast_path_and_limit(engine, oracle):
 def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     """K2's result is a fixed function of the tile: 4- or 8-warp groups, with or without the
     cluster multicast, with or without the cluster-less side launch claiming tiles
-    dynamically, give the same bits."""
+    dynamically, and 2-, 3- or 4-block rectangles give the same bits."""
     torch = torch_mod()
     n = 100003 if p <= 256 else 40001
     D = torch.empty((n, p), dtype=torch.float64, device="cuda")
@@ -539,7 +539,7 @@ def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     pl = plan(n, 30011)
     base = engine.dataset_suffstats(D, schema(p), pl)
     for env in ({"SSTAT_WIDEP_CONSUMERS": "8"}, {"SSTAT_WIDEP_CONSUMERS": "4"}, {"SSTAT_WIDEP_NOCLUSTER": "1"},
-                {"SSTAT_WIDEP_SPARE": "0"}):
+                {"SSTAT_WIDEP_SPARE": "0"}, {"SSTAT_WIDEP_R": "2"}, {"SSTAT_WIDEP_R": "3"}, {"SSTAT_WIDEP_R": "4"}):
         with monkeypatch.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
