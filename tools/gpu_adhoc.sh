@@ -1,2 +1,3 @@
-timeout 1500 python -m pytest tests -q -m gpu -x -k "wide or every_p or widest or c5 or comoments_wide or misaligned or growth" 2>&1 | tail -3 > gpurun_out/pytest_wide.log
-SSTAT_DEBUG=1 timeout 900 python tools/p_sweep.py > gpurun_out/p_sweep.log 2>&1
+for p in 384 512 1024; do
+  for c in 8 4; do SSTAT_DEBUG=1 SSTAT_WIDEP_CONSUMERS=$c timeout 300 python tools/one_case.py $p $(( 8000000000 / (8 * p) )) 3 2>&1 | grep -E "k_widep|^$p" | tail -2 | sed "s/^/C=$c /"; done
+done > gpurun_out/wide_c.log 2>&1
