@@ -1,3 +1,3 @@
-for p in 384 512 1024; do
-  for c in 8 4; do SSTAT_DEBUG=1 SSTAT_WIDEP_CONSUMERS=$c timeout 300 python tools/one_case.py $p $(( 8000000000 / (8 * p) )) 3 2>&1 | grep -E "k_widep|^$p" | tail -2 | sed "s/^/C=$c /"; done
-done > gpurun_out/wide_c.log 2>&1
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py --steps 5 --warmup 3 --config c5 > gpurun_out/bench_c5.log 2>&1
