@@ -1,3 +1,2 @@
-timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py --steps 5 --warmup 3 --config c5 > gpurun_out/bench_c5.log 2>&1
+timeout 1200 python -m pytest tests -q -m gpu -x -k "every_p or misaligned or generated or kats" 2>&1 | tail -3 > gpurun_out/pytest_mid.log
+SSTAT_DEBUG=1 timeout 900 python tools/p_sweep.py > gpurun_out/p_sweep.log 2>&1
