@@ -6,12 +6,12 @@ timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_reference.log 2>&1
 for c in c1 c4 c5; do timeout 900 python bench.py --steps 5 --warmup 3 --config $c > gpurun_out/bench_$c.log 2>&1; done
 timeout 900 python bench.py --impl reference --config c5 --steps 2 --warmup 1 > gpurun_out/bench_reference_c5.log 2>&1
-timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain.log 2>&1 &&
+timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-next > gpurun_out/plain.log 2>&1 &&
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-next > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_smallp -s 2 -c 1 \
-    -o gpurun_out/k1_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_k1.log 2>&1
+    -o gpurun_out/k1_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-next > gpurun_out/ncu_k1.log 2>&1
 timeout 300 python bench.py --steps 2 --warmup 3 --config c5 --no-cpu --no-e2e > gpurun_out/plain_c5.log 2>&1 &&
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_widep -s 1 -c 1 \
-    -o gpurun_out/k2_full -f python bench.py --steps 2 --warmup 3 --config c5 --no-cpu --no-e2e > gpurun_out/ncu_k2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_widep -s 0 -c 1 \
+    -o gpurun_out/k2_full -f python bench.py --steps 2 --warmup 3 --config c5 --no-cpu --no-e2e --no-next > gpurun_out/ncu_k2.log 2>&1
 echo done
