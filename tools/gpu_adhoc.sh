@@ -1,1 +1,1 @@
-timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
+timeout 300 python tools/h2d_probe.py > gpurun_out/h2d.log 2>&1
