@@ -166,13 +166,14 @@ __global__ void k_colsum_final(const ColPart* __restrict__ buf, uint64_t rank_st
 
 // ---------------- co-moments ----------------
 // Per local range: mean_j = c_j + s'_j / n, M2_jk = S'_jk - s'_j s'_k / n from the folded
-// shifted moments (tile partials, the same order as K3a).  One block of 256 per range;
+// shifted moments (tile partials, the same order as K3a).  Blocks over (range, M2 slice);
 // writes [mean(p) | M2(packed)] and n is implicit (range counts).
 __global__ void __launch_bounds__(kTileLanes * 32) k_comoment_range(const double* __restrict__ tp,
                                                         const uint64_t* __restrict__ tile_prefix,
                                                         const uint64_t* __restrict__ range_count,
                                                         const double* __restrict__ shift, uint32_t p, double* out,
-                                                        uint64_t first_range, double* rank_hdr, uint32_t* flags) {
+                                                        uint64_t first_range, double* rank_hdr, uint32_t* flags,
+                                                        uint64_t slice) {
     extern __shared__ double sm[];  // [p] shifted sums, [kTileLanes][32] lanes
     double* ssum = sm;
     double* lanes = sm + p;
@@ -183,8 +184,12 @@ __global__ void __launch_bounds__(kTileLanes * 32) k_comoment_range(const double
     const double n = (double)nr;
     const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
     double* o = out + (uint64_t)r * E;
+    // blockIdx.y = the slice of M2 entries [p + y slice, p + (y + 1) slice); every slice block
+    // folds the p sums (M2 needs them), slice 0 writes the means and the flags
+    const uint64_t x0 = (uint64_t)blockIdx.y * slice, x1 = x0 + slice;
+    const bool lead = blockIdx.y == 0;
     for (int phase = 0; phase < 2; ++phase) {
-        const uint64_t lo = phase == 0 ? 0 : p, hi = phase == 0 ? p : E;
+        const uint64_t lo = phase == 0 ? 0 : p + x0, hi = phase == 0 ? p : (p + x1 < E ? p + x1 : E);
         for (uint64_t e0 = lo; e0 < hi; e0 += 32) {
             const uint64_t e = e0 + le;
             lanes[q * 32 + le] = e < hi ? fold_tiles_lane(tp, E, e, t0, t1, q) : 0.0;  // K3a's order
@@ -195,19 +200,14 @@ __global__ void __launch_bounds__(kTileLanes * 32) k_comoment_range(const double
                 if (phase == 0) {
                     ssum[e] = S;
                     const double c = shift ? shift[(uint64_t)r * p + e] : 0.0;
-                    o[e] = nr ? c + S / n : 0.0;
-                    if (!isfinite(S) || !isfinite(c)) {  // check_chunk (suffstats.cpp:33-45), located later
+                    if (lead) o[e] = nr ? c + S / n : 0.0;
+                    if (lead && (!isfinite(S) || !isfinite(c))) {  // check_chunk (suffstats.cpp:33-45), located later
                         flags[r] = 1;
                         atomicMin(reinterpret_cast<unsigned long long*>(rank_hdr), (unsigned long long)(first_range + r));
                     }
                 } else {
-                    // unpack (j, k) of packed entry e - p
-                    uint32_t i = (uint32_t)(e - p), j = 0, start = 0;
-                    while (start + (p - j) <= i) {
-                        start += p - j;
-                        ++j;
-                    }
-                    const uint32_t k = j + (i - start);
+                    uint32_t j, k;
+                    unpack_index(p, (uint32_t)(e - p), j, k);
                     o[e] = nr ? S - ssum[j] * ssum[k] / n : 0.0;
                 }
             }
@@ -216,52 +216,54 @@ __global__ void __launch_bounds__(kTileLanes * 32) k_comoment_range(const double
     }
 }
 
-// merge_comoments (suffstats.cpp:134-159) over all ranges in ascending order; one block,
-// entries in parallel, ranges sequential.  Range r: [mean p | M2 packed] at
-// range_partial(buf, ...), counts[r] rows.  out: [mean p | M2 packed | rank headers].
-__global__ void __launch_bounds__(1024) k_comoment_merge(const double* __restrict__ buf, uint64_t rank_stride,
-                                                         uint64_t n_ranges, int world,
-                                                         const uint64_t* __restrict__ counts, uint32_t p, double* out) {
-    extern __shared__ double sm[];  // [p] delta
-    double* delta = sm;
+// merge_comoments (suffstats.cpp:134-159) over all ranges in ascending order: blocks over the
+// M2 entries, ranges sequential.  Every block runs the same mean chain (the p means and the
+// deltas, bit-identical across blocks), so each entry sees exactly the single-block sequence
+// of operations.  Range r: [mean p | M2 packed] at range_partial(buf, ...), counts[r] rows.
+// out: [mean p | M2 packed | rank headers] (block 0 writes the means and headers).
+__global__ void __launch_bounds__(256) k_comoment_merge(const double* __restrict__ buf, uint64_t rank_stride,
+                                                        uint64_t n_ranges, int world,
+                                                        const uint64_t* __restrict__ counts, uint32_t p, double* out) {
+    extern __shared__ double sm[];  // [p] mean, [p] delta
+    double* mean = sm;
+    double* delta = sm + p;
     const uint64_t E = partial_len(p), NP = E - p;
-    double* mean = out;
     double* m2 = out + p;
-    if (threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
         out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // this thread's M2 entry
+    const bool has = i < NP;
+    uint32_t j = 0, k = 0;
+    if (has) unpack_index(p, (uint32_t)i, j, k);
+    double acc = 0.0;
     uint64_t na = 0;
-    for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) mean[j] = 0.0;
-    for (uint64_t i = threadIdx.x; i < NP; i += blockDim.x) m2[i] = 0.0;
+    for (uint32_t c = threadIdx.x; c < p; c += blockDim.x) mean[c] = 0.0;
     __syncthreads();
     for (uint64_t r = 0; r < n_ranges; ++r) {
         const uint64_t nb = counts[r];
         if (nb == 0) continue;  // b.n == 0: a unchanged
         const double* pb = range_partial(buf, rank_stride, n_ranges, world, E, r);
         if (na == 0) {  // a.n == 0: a = b
-            for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) mean[j] = pb[j];
-            for (uint64_t i = threadIdx.x; i < NP; i += blockDim.x) m2[i] = pb[p + i];
+            for (uint32_t c = threadIdx.x; c < p; c += blockDim.x) mean[c] = pb[c];
+            if (has) acc = pb[p + i];
             na = nb;
             __syncthreads();
             continue;
         }
         const double dna = (double)na, dnb = (double)nb, dn = dna + dnb;
-        for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) delta[j] = __dsub_rn(pb[j], mean[j]);
+        for (uint32_t c = threadIdx.x; c < p; c += blockDim.x) delta[c] = __dsub_rn(pb[c], mean[c]);
         __syncthreads();
         const double scale = __ddiv_rn(__dmul_rn(dna, dnb), dn);
-        for (uint64_t i = threadIdx.x; i < NP; i += blockDim.x) {
-            uint32_t j = 0, start = 0;
-            while (start + (p - j) <= i) {
-                start += p - j;
-                ++j;
-            }
-            const uint32_t k = j + (uint32_t)(i - start);
-            m2[i] = __dadd_rn(__dadd_rn(m2[i], pb[p + i]), __dmul_rn(__dmul_rn(delta[j], delta[k]), scale));
-        }
+        if (has) acc = __dadd_rn(__dadd_rn(acc, pb[p + i]), __dmul_rn(__dmul_rn(delta[j], delta[k]), scale));
         const double frac = __ddiv_rn(dnb, dn);
-        for (uint32_t j = threadIdx.x; j < p; j += blockDim.x) mean[j] = __dadd_rn(mean[j], __dmul_rn(delta[j], frac));
+        __syncthreads();  // every thread has read delta / mean before the means move
+        for (uint32_t c = threadIdx.x; c < p; c += blockDim.x) mean[c] = __dadd_rn(mean[c], __dmul_rn(delta[c], frac));
         na += nb;
         __syncthreads();
     }
+    if (has) m2[i] = acc;
+    if (blockIdx.x == 0)
+        for (uint32_t c = threadIdx.x; c < p; c += blockDim.x) out[c] = mean[c];
 }
 
 }  // namespace
@@ -310,19 +312,24 @@ cudaError_t launch_comoment_range(const double* tile_partials, const uint64_t* t
         cudaError_t e = cudaFuncSetAttribute(k_comoment_range, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_comoment_range<<<n_ranges, kTileLanes * 32, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, p, out,
-                                                      first_range, rank_hdr, flags);
+    const uint64_t cross = (uint64_t)p * (p + 1) / 2;
+    const uint64_t slice = 32ull * ((p + 31) / 32);  // as K3a: the redundant sums fold <= the slice
+    const dim3 grid(n_ranges, (unsigned)((cross + slice - 1) / slice));
+    k_comoment_range<<<grid, kTileLanes * 32, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, p, out,
+                                                              first_range, rank_hdr, flags, slice);
     return cudaGetLastError();
 }
 
 cudaError_t launch_comoment_merge(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world,
                                   const uint64_t* counts, uint32_t p, double* out, cudaStream_t stream) {
-    const size_t smem = p * sizeof(double);
+    const size_t smem = 2 * p * sizeof(double);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_comoment_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_comoment_merge<<<1, 1024, smem, stream>>>(buf, rank_stride, n_ranges, world, counts, p, out);
+    const uint64_t np = (uint64_t)p * (p + 1) / 2;
+    k_comoment_merge<<<(unsigned)((np + 255) / 256), 256, smem, stream>>>(buf, rank_stride, n_ranges, world, counts, p,
+                                                                          out);
     return cudaGetLastError();
 }
 

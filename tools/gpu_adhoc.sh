@@ -1,2 +1,3 @@
-timeout 1500 python -m pytest tests -q -m gpu -x -k "kats or table1 or generated or nonfinite or every_source or glue or c1 or widest or sharded or binary32 or column_sum" 2>&1 | tail -3 > gpurun_out/pytest_ref.log
-timeout 600 python tools/refexact_probe.py > gpurun_out/refexact.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x -k "comoments or glue" 2>&1 | tail -3 > gpurun_out/pytest_cm.log
+timeout 600 python bench.py --steps 5 --warmup 3 --config c5 --no-cpu --no-e2e > gpurun_out/bench_c5_cm.log 2>&1
+timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_c2_cm.log 2>&1
