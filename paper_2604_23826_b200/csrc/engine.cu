@@ -630,7 +630,8 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             j.claim = c->d_claim.as<unsigned long long>();
         }
         uint32_t kernels = 1;
-        CUDA_TRY(wide ? launch_widep(j, c->sms, s, &kernels) : launch_smallp(j, c->sms, s));
+        CUDA_TRY(wide ? (splitp_handles(p) ? launch_splitp(j, c->sms, s) : launch_widep(j, c->sms, s, &kernels))
+                      : launch_smallp(j, c->sms, s));
         if (tm) tm->kernel_launches += kernels - 1;  // the callers count one accumulate kernel
     };
 

@@ -1,0 +1,243 @@
+// k_splitp.cu — K1w: 64 < p <= 128, K1's register-direct DMMA pass with the triangle split
+// over W warps.
+//
+// Replaces accumulate_into<double> (reference src/suffstats.cpp:50-70) at these widths.  K2's
+// rectangles pad the 9-16-block triangle and stream it through a cluster-wide shared-memory
+// ring; here the CTA's 8 warps form 8/W row groups of W warps: the W warps of a group read the
+// same 4-row k-steps straight from global memory (the group's other warps hit L1/L2), each
+// keeps the accumulators of every W-th block of the NB(NB+1)/2-block triangle (block b with
+// b % W == part, chosen at compile time so no DMMA is predicated) and part 0 adds the column
+// sums.  At the end of a tile the groups' partials meet in shared memory and are added in
+// group order into the canonical tile partial.  Tiles are widep_tile_rows(p) rows (as K2),
+// so the choice between the two kernels never changes the tile partition.
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sstat_b200 {
+namespace {
+
+constexpr int kU = 2;  // k-steps of loads in flight per warp
+
+template <int NB>
+struct SplitP {
+    static constexpr int NBLK = NB * (NB + 1) / 2;
+    static constexpr int FRAG = NBLK * 64 + NB * 8;  // per-group epilogue values
+};
+
+template <int NB, int W, int PART>
+struct Mine {  // blocks b = PART, PART + W, ... of the canonical (J <= K) enumeration
+    static constexpr int N = (SplitP<NB>::NBLK - PART + W - 1) / W;
+};
+
+template <int NB>
+__device__ __forceinline__ void load_k(const double* __restrict__ rowp, int g, uint32_t p, double (&x)[NB]) {
+#pragma unroll
+    for (int J = 0; J < NB; ++J) {
+        const int c = 8 * J + g;
+        x[J] = c < (int)p ? __ldg(rowp + c) : 0.0;
+    }
+}
+
+template <int NB, int W, int PART>
+__device__ __forceinline__ void split_step(const double (&x)[NB], const double (&c)[NB],
+                                           double (&acc)[Mine<NB, W, PART>::N][2], double (&s)[NB]) {
+    double d[NB];
+#pragma unroll
+    for (int J = 0; J < NB; ++J) {
+        d[J] = x[J] - c[J];
+        if (PART == 0) s[J] += d[J];
+    }
+    int b = 0;
+#pragma unroll
+    for (int J = 0; J < NB; ++J)
+#pragma unroll
+        for (int K = J; K < NB; ++K, ++b)
+            if (b % W == PART) dmma_8x8x4(acc[b / W][0], acc[b / W][1], d[J], d[K]);
+}
+
+// Canonical destination of epilogue value e (block values, then the sums) or -1
+// (padding / lower mirror of a diagonal block); columns col(J, g) = 8 J + g.
+template <int NB>
+__device__ int split_slot(int e, uint32_t p) {
+    constexpr int NBLK = SplitP<NB>::NBLK;
+    if (e < NBLK * 64) {
+        int b = e >> 6;
+        const int l = (e & 63) >> 1, m = l >> 2, n = 2 * (l & 3) + (e & 1);
+        int J = 0;
+        while (b >= NB - J) {
+            b -= NB - J;
+            ++J;
+        }
+        const int K = J + b;
+        const int a = 8 * J + m, bb = 8 * K + n;
+        if (a >= (int)p || bb >= (int)p) return -1;
+        if (J == K && a > bb) return -1;
+        return (int)(p + packed_index(p, a < bb ? a : bb, a < bb ? bb : a));
+    }
+    const int e2 = e - NBLK * 64;
+    const int a = 8 * (e2 >> 3) + (e2 & 7);
+    return a < (int)p ? a : -1;
+}
+
+template <int NB, int W, int PART>
+__device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_rows, double* red) {
+    using C = SplitP<NB>;
+    constexpr int G = kWarps / W;  // row groups
+    constexpr int NM = Mine<NB, W, PART>::N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int group = warp / W;
+    const int g = lane >> 2, kk = lane & 3;
+    const uint32_t p = job.p;
+    const uint64_t E = partial_len(p);
+
+    for (uint64_t t = job.tile_begin + blockIdx.x; t < job.tile_end; t += gridDim.x) {
+        const uint32_t r = range_of_tile(job.tile_prefix, job.n_ranges, t);
+        const uint64_t rs = __ldg(job.range_start + r), rc = __ldg(job.range_count + r);
+        const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + r)) * tile_rows;
+        const uint64_t left = rs + rc - row0;
+        const uint32_t rows = left < tile_rows ? (uint32_t)left : tile_rows;
+        const double* __restrict__ tile = job.base + (row0 - job.base_row) * p;
+        const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p : nullptr;
+        double c[NB];
+#pragma unroll
+        for (int J = 0; J < NB; ++J) c[J] = (crow != nullptr && 8 * J + g < (int)p) ? crow[8 * J + g] : 0.0;
+        double acc[NM][2], s[NB];
+#pragma unroll
+        for (int b = 0; b < NM; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+        for (int J = 0; J < NB; ++J) s[J] = 0.0;
+
+        const uint32_t nks = rows >> 2;
+        const uint64_t kstride = (uint64_t)G * 4 * p;
+        uint32_t ks = group;
+        const double* rowp = tile + (uint64_t)(group * 4 + kk) * p;
+        for (; ks + G * (kU - 1) < nks; ks += G * kU, rowp += kU * kstride) {
+            double x[kU][NB];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) load_k<NB>(rowp + u * kstride, g, p, x[u]);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) split_step<NB, W, PART>(x[u], c, acc, s);
+        }
+        for (; ks < nks; ks += G, rowp += kstride) {
+            double x[NB];
+            load_k<NB>(rowp, g, p, x);
+            split_step<NB, W, PART>(x, c, acc, s);
+        }
+        // ragged tail (rows % 4): the group whose turn k-step nks is; missing rows add 0
+        if ((rows & 3) && group == (int)(nks % G)) {
+            const uint32_t row = nks * 4 + kk;
+            double x[NB];
+            if (row < rows) {
+                load_k<NB>(tile + (uint64_t)row * p, g, p, x);
+            } else {
+#pragma unroll
+                for (int J = 0; J < NB; ++J) x[J] = c[J];
+            }
+            split_step<NB, W, PART>(x, c, acc, s);
+        }
+
+        // ---- epilogue: each group's partial into red[group], then the groups in order ----
+        double* mine = red + group * C::FRAG;
+        {
+            int b = 0;
+#pragma unroll
+            for (int J = 0; J < NB; ++J)
+#pragma unroll
+                for (int K = J; K < NB; ++K, ++b)
+                    if (b % W == PART) {
+                        mine[b * 64 + lane * 2] = acc[b / W][0];
+                        mine[b * 64 + lane * 2 + 1] = acc[b / W][1];
+                    }
+        }
+        if (PART == 0) {
+#pragma unroll
+            for (int J = 0; J < NB; ++J) {
+                s[J] += __shfl_xor_sync(0xffffffffu, s[J], 1);
+                s[J] += __shfl_xor_sync(0xffffffffu, s[J], 2);
+            }
+            if (kk == 0) {
+#pragma unroll
+                for (int J = 0; J < NB; ++J) mine[C::NBLK * 64 + J * 8 + g] = s[J];
+            }
+        }
+        __syncthreads();
+        double* out = job.tile_partials + t * E;
+        for (int e = threadIdx.x; e < C::FRAG; e += kThreads) {
+            const int slot = split_slot<NB>(e, p);
+            if (slot < 0) continue;
+            double v = red[e];
+#pragma unroll
+            for (int q = 1; q < G; ++q) v += red[q * C::FRAG + e];
+            out[slot] = v;
+        }
+        __syncthreads();
+    }
+}
+
+template <int NB, int W>
+__global__ void __launch_bounds__(kThreads, 1) k_splitp(TileJob job, uint32_t tile_rows) {
+    extern __shared__ double red[];  // [8 / W][FRAG]
+    const int part = (threadIdx.x >> 5) % W;
+    if (part == 0) split_body<NB, W, 0>(job, tile_rows, red);
+    else if (part == 1) split_body<NB, W, 1>(job, tile_rows, red);
+    else if constexpr (W > 2) {
+        if (part == 2) split_body<NB, W, 2>(job, tile_rows, red);
+        else split_body<NB, W, 3>(job, tile_rows, red);
+    }
+}
+
+template <int NB, int W>
+cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
+    constexpr size_t smem = sizeof(double) * (kWarps / W) * SplitP<NB>::FRAG;
+    static std::atomic<int> cached[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = dev < 64 ? cached[dev].load() : 0;
+    if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_splitp<NB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_splitp<NB, W>, kThreads, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) per_sm = 1;
+        if (getenv("SSTAT_DEBUG")) fprintf(stderr, "k_splitp<%d,%d>: smem=%zu per_sm=%d\n", NB, W, smem, per_sm);
+        if (dev < 64) cached[dev].store(per_sm);
+    }
+    const uint64_t tiles = job.tile_end - job.tile_begin;
+    const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
+    if (grid == 0) return cudaSuccess;
+    k_splitp<NB, W><<<(unsigned)grid, kThreads, smem, stream>>>(job, widep_tile_rows(job.p));
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// Measured (profiles/r01_p_sweep.log): W = 2 for NB = 9..11 (21-22 TF/s vs K2's 8.5-17.5),
+// W = 4 for NB = 13..16 (20-22 TF/s vs 14-21); at NB = 12 both splits stay near 14 TF/s and
+// K2's 2x2 rectangles do better (16), so p = 89..96 keeps K2.
+bool splitp_handles(uint32_t p) {
+    if (const char* env = getenv("SSTAT_SPLITP")) {
+        if (atoi(env) == 0) return false;
+    }
+    const uint32_t nb = (p + 7) / 8;
+    return p > 64 && p <= 128 && nb != 12;
+}
+
+cudaError_t launch_splitp(const TileJob& job, int sms, cudaStream_t stream) {
+    switch ((job.p + 7) / 8) {
+        case 9: return launch_nb<9, 2>(job, sms, stream);
+        case 10: return launch_nb<10, 2>(job, sms, stream);
+        case 11: return launch_nb<11, 2>(job, sms, stream);
+        case 13: return launch_nb<13, 4>(job, sms, stream);
+        case 14: return launch_nb<14, 4>(job, sms, stream);
+        case 15: return launch_nb<15, 4>(job, sms, stream);
+        case 16: return launch_nb<16, 4>(job, sms, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sstat_b200

@@ -12,6 +12,11 @@ namespace sstat_b200 {
 // min(tiles, sms x resident CTAs per SM).
 cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream);
 
+// K1w: 64 < p <= 128 (splitp_handles), K1's register-direct pass with the triangle split over
+// warps; tiles of widep_tile_rows(p) rows like K2.
+bool splitp_handles(uint32_t p);
+cudaError_t launch_splitp(const TileJob& job, int sms, cudaStream_t stream);
+
 // K2: tiles for p > 64 (smem-staged DMMA SYRK), tiles of widep_tile_rows(p) rows.
 // *kernels (optional) receives the number of kernels launched (2 when the idle-slot split runs).
 cudaError_t launch_widep(const TileJob& job, int sms, cudaStream_t stream, uint32_t* kernels = nullptr);

@@ -533,6 +533,7 @@ def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     cluster multicast, with or without the cluster-less side launch claiming tiles
     dynamically, and 2-, 3- or 4-block rectangles give the same bits."""
     torch = torch_mod()
+    monkeypatch.setenv("SSTAT_SPLITP", "0")  # K2 itself at every p (K1w takes 64 < p <= 128 by default)
     n = 100003 if p <= 256 else 40001
     D = torch.empty((n, p), dtype=torch.float64, device="cuda")
     engine.generate(D, 2, 7, 1.5, 0, 0, n, p)
