@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_splitp(TileJob job, uint32_t ti
     const int part = (threadIdx.x >> 5) % W;
     if (part == 0) split_body<NB, W, 0>(job, tile_rows, red);
     else if (part == 1) split_body<NB, W, 1>(job, tile_rows, red);
-    else if constexpr (W > 2) {
+    else if constexpr (W == 4) {
         if (part == 2) split_body<NB, W, 2>(job, tile_rows, red);
         else split_body<NB, W, 3>(job, tile_rows, red);
     }

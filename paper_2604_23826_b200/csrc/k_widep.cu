@@ -674,7 +674,10 @@ uint32_t choose_r(uint32_t nb, uint32_t consumers) {
     for (uint32_t R : {4u, 3u, 2u}) {
         const uint32_t nr = (nb + R - 1) / R, items = nr * (nr + 1) / 2;
         const uint32_t slots = (items + consumers - 1) / consumers * consumers;
-        const double cost = slots * (R * R + R / 4.0) / (nb * (nb + 1) / 2.0);
+        // 2x2 rectangles load one fragment per DMMA and need twice the groups per tile: measured
+        // 15-25 % below this model from p = 136 on (profiles/r01_p_sweep.log), hence the 1.25
+        // (not at nb <= 12, where they measured best)
+        const double cost = slots * (R * R + R / 4.0) / (nb * (nb + 1) / 2.0) * (R == 2 && nb > 12 ? 1.25 : 1.0);
         if (best_cost == 0 || cost < 0.97 * best_cost) best = R, best_cost = cost;
     }
     return best;
