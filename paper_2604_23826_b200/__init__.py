@@ -24,6 +24,7 @@ from .sstat import (  # noqa: F401
     accumulate_chunk,
     dataset_suffstats,
     default_engine,
+    fold_range_partials,
     merge_suffstats,
     packed_index,
     plan_partitions,

@@ -427,6 +427,28 @@ class Engine:
         self.last_timings = tm
         return out
 
+    def range_partials(self, dataset, schema: DatasetSchema, plan: ReductionPlan, first_range: int,
+                       last_range: int, flags: int = 0, first_row: int = 0,
+                       n_rows: Optional[int] = None) -> np.ndarray:
+        """Per-range partials [sums | packed cross] of ranges [first_range, last_range) in raw space,
+        without the fold: what a rank contributes to the exchange, or a checkpoint of finished
+        ranges (run_reduction's partials slots, reduce.hpp:85,108).  Shape (last - first, E)."""
+        schema.validate()
+        p = schema.column_count()
+        src, keep = self._source(dataset, p, first_row, n_rows)
+        starts, counts = plan.partition.arrays()
+        E = p + p * (p + 1) // 2
+        out = np.zeros((max(last_range - first_range, 0), E))
+        err = N.Error()
+        st = self._lib.sstat_cuda_range_partials(self._ctx, ctypes.byref(src), p, starts.ctypes.data,
+                                                 counts.ctypes.data, len(starts), first_range, last_range,
+                                                 int(plan.precision), flags,
+                                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(err))
+        del keep
+        if st != N.OK:
+            _raise(st, err, in_dataset=True)
+        return out
+
     def _source(self, dataset, p: int, first_row: int, n_rows: Optional[int]):
         src = N.Source()
         if isinstance(dataset, (str, os.PathLike)):
@@ -546,6 +568,33 @@ def accumulate_chunk(chunk: Chunk, schema: DatasetSchema,
 def dataset_suffstats(dataset, schema: DatasetSchema, plan: ReductionPlan,
                       timings: Optional[ReductionTimings] = None) -> SuffStats:
     return default_engine().dataset_suffstats(dataset, schema, plan, timings)
+
+
+def fold_range_partials(partials: np.ndarray, schema: DatasetSchema, plan: ReductionPlan,
+                        flags: int = 0) -> SuffStats:
+    """The dataset result from all R ranges' partials (R x E, range order) — e.g. checkpointed
+    pieces from range_partials — folded on the host in the device's own order (fast mode: the
+    8-lane fold; SSTAT_FLAG_REFEXACT / Binary32Diagnostic: the reference's ascending fold), so it
+    is bit-identical to dataset_suffstats over the same plan."""
+    schema.validate()
+    p = schema.column_count()
+    R = len(plan.partition.ranges)
+    E = p + p * (p + 1) // 2
+    parts = np.ascontiguousarray(partials, dtype=np.float64).reshape(-1)
+    if parts.size != R * E:
+        raise ValueError(f"expected {R} x {E} partials, got {parts.size} values")
+    buf = np.concatenate([np.full(4, np.nan), parts])  # one rank: [4-double header | R x E]
+    res = np.zeros(E)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = N.load().sstat_fold_ranges_host(buf.ctypes.data_as(dp), 4 + R * E, R, 1, p, int(plan.precision), flags,
+                                         res.ctypes.data_as(dp))
+    if st != N.OK:
+        raise ValueError(N.status_string(st))
+    out = SuffStats.empty(schema, plan.precision)
+    out.n = plan.partition.total_rows()
+    out.sums[:] = res[:p]
+    out.cross[:] = res[p:]
+    return out
 
 
 def shard_ranges(n_ranges: int, rank: int, world: int):

@@ -291,6 +291,29 @@ def test_sharded_partials_fold_bit_identical(engine, oracle, W):
     assert np.array_equal(bits(res[p:]), bits(whole.cross))
 
 
+@pytest.mark.parametrize("flags", [0, 2])
+def test_checkpoint_resume_partials(engine, flags):
+    """Checkpoint / resume: per-range partials of a first part of the plan and of the rest,
+    computed in separate calls from separate row shards, fold on the host to the bits of one
+    dataset_suffstats pass (fast mode and reference order)."""
+    from paper_2604_23826_b200 import fold_range_partials
+
+    torch = torch_mod()
+    n, p, chunk = 250_003, 24, 7001
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 0, 17, 1.0, 2, 0, n, p)
+    pl = plan(n, chunk)
+    whole = engine.dataset_suffstats(D, schema(p), pl, flags=flags)
+    R = len(pl.partition.ranges)
+    k = R // 3
+    split_row = pl.partition.ranges[k].start_row
+    first = engine.range_partials(D[:split_row].contiguous(), schema(p), pl, 0, k, flags=flags, n_rows=split_row)
+    rest = engine.range_partials(D[split_row:].contiguous(), schema(p), pl, k, R, flags=flags, first_row=split_row,
+                                 n_rows=n - split_row)
+    resumed = fold_range_partials(np.concatenate([first, rest]), schema(p), pl, flags=flags)
+    assert resumed.bit_equal(whole)
+
+
 def test_nccl_world1_identical(oracle):
     """The NCCL exchange path with a communicator of one rank."""
     from paper_2604_23826_b200 import Engine
