@@ -29,6 +29,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/sstat_cuda.h"
 #include "common.cuh"
@@ -90,6 +91,15 @@ struct HostBuf {
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+
+// NVTX ranges around each ABI call and its phases (host-side enqueue timeline for nsys / ncu
+// range replay; header-only NVTX3, no cost without an attached tool).
+struct Trace {
+    explicit Trace(const char* name) { nvtxRangePushA(name); }
+    ~Trace() { nvtxRangePop(); }
+    Trace(const Trace&) = delete;
+    Trace& operator=(const Trace&) = delete;
+};
 
 // Host feeder threads (the loader half of reference src/binfile.cpp:140-161 read_rows): a
 // staging slot is filled by parallel page-cache reads / memcpys of disjoint row blocks, so
@@ -565,6 +575,8 @@ uint64_t* upload_meta(sstat_cuda_ctx* c, Plan& P, uint64_t TR, cudaStream_t s) {
 void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
          sstat_cuda_timings* tm) {
     BinFile file;
+    Trace trace_run(P.mode == Mode::Comoments ? "sstat.comoments" : P.mode == Mode::Partials ? "sstat.range_partials"
+                    : P.mode == Mode::Chunk ? "sstat.accumulate_chunk" : "sstat.dataset");
     check_plan(c, src, P, file);
     const int world = (P.mode == Mode::Dataset || P.mode == Mode::Comoments) ? c->world : 1;
     const bool comoments = P.mode == Mode::Comoments;  // co-moments always take the shifted fast path
@@ -791,6 +803,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     }
 
     // ---- exchange (rank-ordered all-gather of per-range partials) ----
+    Trace trace_tail("sstat.exchange+fold+readback");
     const double* fold_buf = rank_buf;
     if (world > 1) {
         CUDA_TRY(c->d_gather.reserve(rank_stride * world * 8));
@@ -862,6 +875,7 @@ struct ColResult {
 };
 
 void run_colsum(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32_t column, ColResult& res) {
+    Trace trace_run("sstat.column_sum");
     BinFile file;
     check_plan(c, src, P, file);
     if (column >= P.p)
