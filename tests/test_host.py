@@ -190,3 +190,23 @@ def test_host_fast_fold_is_the_8_lane_order(oracle, W):
             t += s
         want[e] = t
     assert np.array_equal(bits(out), bits(want))
+
+
+def test_fold_range_partials_resume_equals_reference(oracle):
+    """fold_range_partials (the resume half of checkpoint/resume) over the reference's own
+    per-range partials gives the reference's dataset result bit-for-bit in reference order,
+    and rejects a partial set of the wrong size."""
+    from paper_2604_23826_b200 import DatasetSchema, ReductionPlan, fold_range_partials, plan_partitions
+
+    p, n, chunk = 6, 2500, 173
+    X = oracle.generate(0, 9, 1.0, 2, 0, n, p)
+    s, c = oracle.plan_partitions(n, chunk)
+    parts = [np.concatenate(oracle.accumulate_chunk(X[int(a): int(a + b)], p, int(a))[1:]) for a, b in zip(s, c)]
+    plan = ReductionPlan(plan_partitions(n, chunk))
+    schema = DatasetSchema.generic(p, False)
+    got = fold_range_partials(np.array(parts), schema, plan, flags=2)
+    want = oracle.run_reduction(X, p, s, c, 1)
+    assert got.n == n
+    assert np.array_equal(bits(got.sums), bits(want[1])) and np.array_equal(bits(got.cross), bits(want[2]))
+    with pytest.raises(ValueError):
+        fold_range_partials(np.array(parts[:-1]), schema, plan)
