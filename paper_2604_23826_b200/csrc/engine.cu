@@ -215,6 +215,11 @@ struct sstat_cuda_ctx {
     // host feeder for pageable / file sources (created on first use)
     unsigned host_threads = 0;  // 0 = default_host_threads()
     std::unique_ptr<FillPool> pool;
+    // CUDA graph of the last device-resident K1 pass (gather, K1, K3a, K3b, read-back), replayed
+    // while every input of the captured launches is unchanged (graph_key)
+    cudaStream_t cap = nullptr;  // private capture stream (the caller's stream is never captured)
+    cudaGraphExec_t graph = nullptr;
+    std::vector<uint64_t> graph_key;
 };
 
 namespace {
@@ -647,10 +652,78 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         if (tm) tm->kernel_launches += kernels - 1;  // the callers count one accumulate kernel
     };
 
-    CUDA_TRY(cudaEventRecord(c->ev[0], s));
-    if (tm) tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
+    // ---- K1 on a resident shard, one GPU: the whole pass as one replayed CUDA graph ----
+    // (launch-bound for small shards: four kernels, five events and the read-back become one
+    // cudaGraphLaunch; captured on a private stream, keyed by every input the launches bake in)
+    const bool graphable = src->kind == SSTAT_SRC_DEVICE && world == 1 && P.mode == Mode::Dataset && !refexact &&
+                           !wide && L > 0 && nt > 0 && !getenv("SSTAT_NO_GRAPH");
+    if (graphable) {
+        CUDA_TRY(c->h_result.reserve(E * 8 + kHdr * 8));
+        CUDA_TRY(c->d_result.reserve((E + kHdr) * 8));  // K3b appends the rank header
+        const double* base = static_cast<const double*>(src->ptr);
+        const std::vector<uint64_t> key = {
+            (uint64_t)(uintptr_t)base, src->first_row, p, L, nt, E, P.r0, shift, (uint64_t)(uintptr_t)s,
+            c->d_meta.gen, c->d_tiles.gen, c->d_rank.gen, c->d_flags.gen, c->d_shift.gen, c->d_result.gen,
+            (uint64_t)(uintptr_t)c->h_result.p, (uint64_t)(uintptr_t)c->d_meta.p, (uint64_t)(uintptr_t)c->d_tiles.p,
+            (uint64_t)(uintptr_t)c->d_rank.p, (uint64_t)(uintptr_t)c->d_shift.p, (uint64_t)(uintptr_t)c->d_result.p};
+        if (!(c->graph && c->graph_key == key)) {
+            if (c->graph) cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+            c->graph_key.clear();
+            CUDA_TRY(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeRelaxed));
+            cudaGraph_t g = nullptr;
+            try {
+                const cudaStream_t cs = c->cap;
+                if (shift)
+                    CUDA_TRY(launch_gather_shift(base, src->first_row, d_starts, d_counts, (uint32_t)L, p,
+                                                 c->d_shift.as<double>(), cs));
+                CUDA_TRY(cudaEventRecordWithFlags(c->ev[0], cs, cudaEventRecordExternal));
+                TileJob j{};
+                j.base = base;
+                j.base_row = src->first_row;
+                j.range_start = d_starts;
+                j.range_count = d_counts;
+                j.tile_prefix = d_prefix;
+                j.shift = d_shift;
+                j.n_ranges = (uint32_t)L;
+                j.p = p;
+                j.tile_begin = 0;
+                j.tile_end = nt;
+                j.tile_partials = c->d_tiles.as<double>();
+                CUDA_TRY(launch_smallp(j, c->sms, cs));
+                CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
+                CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
+                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, cs));
+                CUDA_TRY(cudaEventRecordWithFlags(c->ev[2], cs, cudaEventRecordExternal));
+                CUDA_TRY(cudaEventRecordWithFlags(c->ev[3], cs, cudaEventRecordExternal));
+                CUDA_TRY(launch_final_fold(rank_buf, rank_stride, P.R, 1, p, 0u, false, c->d_result.as<double>(), cs));
+                CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
+                CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + kHdr) * 8, cudaMemcpyDeviceToHost, cs));
+            } catch (...) {
+                cudaStreamEndCapture(c->cap, &g);
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                throw;
+            }
+            CUDA_TRY(cudaStreamEndCapture(c->cap, &g));
+            const cudaError_t ie = cudaGraphInstantiate(&c->graph, g, 0);
+            cudaGraphDestroy(g);
+            CUDA_TRY(ie);
+            c->graph_key = key;
+        }
+        CUDA_TRY(cudaGraphLaunch(c->graph, s));
+        if (tm) {
+            tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
+            tm->kernel_launches += shift ? 4 : 3;
+        }
+    }
+
+    if (!graphable) CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    if (!graphable && tm) tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
     bool scanned = false;  // the non-finite scan already ran for this rank
-    if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
+    if (graphable) {
+        // everything up to the read-back is in the graph
+    } else if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
         const double* base = static_cast<const double*>(src->ptr);
         const uint64_t base_row = src->first_row;
         if (refexact) {
@@ -805,6 +878,9 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     // ---- exchange (rank-ordered all-gather of per-range partials) ----
     Trace trace_tail("sstat.exchange+fold+readback");
     const double* fold_buf = rank_buf;
+    if (graphable) {
+        // folds and read-back are in the graph
+    } else {
     if (world > 1) {
         CUDA_TRY(c->d_gather.reserve(rank_stride * world * 8));
         ncclResult_t r = ncclAllGather(rank_buf, c->d_gather.p, rank_stride, ncclDouble, c->comm, s);
@@ -828,9 +904,10 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     if (tm) tm->kernel_launches += 1;
     CUDA_TRY(cudaEventRecord(c->ev[4], s));
     CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
-    double* hres = c->h_result.as<double>();
     // result and every rank's header in one read-back (K3b appends the headers)
-    CUDA_TRY(cudaMemcpyAsync(hres, c->d_result.p, (E + world * kHdr) * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + world * kHdr) * 8, cudaMemcpyDeviceToHost, s));
+    }
+    double* hres = c->h_result.as<double>();
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
     if (!scanned && world == 1 && L > 0) {
@@ -1026,6 +1103,10 @@ int sstat_cuda_init(sstat_cuda_ctx** out, int device) {
         return SSTAT_ERR_CUDA;
     }
     c->stream = c->own;
+    if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return SSTAT_ERR_CUDA;
+    }
     for (auto& e : c->ev)
         if (cudaEventCreate(&e) != cudaSuccess) {
             delete c;
@@ -1051,8 +1132,10 @@ int sstat_cuda_destroy(sstat_cuda_ctx* c) {
         for (auto e : c->ev_copied) cudaEventDestroy(e);
         for (auto e : c->ev_free) cudaEventDestroy(e);
         for (auto e : c->ev) cudaEventDestroy(e);
+        if (c->graph) cudaGraphExecDestroy(c->graph);
         cudaStreamDestroy(c->own);
         cudaStreamDestroy(c->copy);
+        cudaStreamDestroy(c->cap);
     }
     delete c;
     return SSTAT_OK;
