@@ -586,3 +586,44 @@ def test_c5_scale_wide(engine):
     assert sums_err(fast.sums, exact.sums, exact.cross, n, p) <= TOL
     del D
     torch.cuda.empty_cache()
+
+
+def test_concurrent_engines_threads():
+    """Two contexts driven from two host threads at once (K1, K1w and K2 widths, device and
+    host sources, K2's shared plan cache and side stream) give the same bits as one at a time."""
+    import threading
+
+    from paper_2604_23826_b200 import Engine
+
+    torch = torch_mod()
+    cases = [(16, 200_003), (256, 60_001), (104, 50_001), (72, 40_003)]
+    data = []
+    e0 = Engine(0)
+    for p, n in cases:
+        D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+        e0.generate(D, 2, 31, 0.5, 0, 0, n, p)
+        data.append((D, p, n))
+    want = [e0.dataset_suffstats(D, schema(p), plan(n, 30_011)) for D, p, n in data]
+    got = {}
+    errors = []
+
+    def worker(tid):
+        try:
+            e = Engine(0)
+            for rep in range(3):
+                for i, (D, p, n) in enumerate(data):
+                    src = D if (i + tid + rep) % 2 == 0 else D.cpu().numpy()
+                    got[(tid, rep, i)] = e.dataset_suffstats(src, schema(p), plan(n, 30_011))
+            e.close()
+        except Exception as ex:  # pragma: no cover - reported below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (tid, rep, i), ss in got.items():
+        assert ss.bit_equal(want[i]), (tid, rep, i)
+    e0.close()
