@@ -144,10 +144,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             c_int,
             [c_void_p, c_void_p, c_uint64, c_uint32, c_uint64, c_uint32, c_uint32, u64p, dp, dp, P(Error)],
         ),
-        "sstat_cuda_dataset": (
+        "sstat_cuda_dataset": (  # sums_out / cross_out as addresses (the hot call passes ints)
             c_int,
-            [c_void_p, P(Source), c_uint32, c_void_p, c_void_p, c_uint64, c_uint32, c_uint32, u64p, dp, dp,
-             P(Timings), P(Error)],
+            [c_void_p, P(Source), c_uint32, c_void_p, c_void_p, c_uint64, c_uint32, c_uint32, u64p, c_void_p,
+             c_void_p, P(Timings), P(Error)],
         ),
         "sstat_cuda_range_partials": (
             c_int,

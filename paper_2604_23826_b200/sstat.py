@@ -107,14 +107,21 @@ class Partition:
 
     def arrays(self):
         """(starts, counts) as uint64 arrays for the C ABI, cached while the ranges are unchanged."""
+        return self._cached()[1:3]
+
+    def addresses(self):
+        """(starts address, counts address, n) of the cached arrays (the hot call's arguments)."""
+        return self._cached()[3]
+
+    def _cached(self):
         key = (id(self.ranges), len(self.ranges), self.ranges[-1] if self.ranges else None)
         cached = getattr(self, "_arrays", None)
         if cached is None or cached[0] != key:
             starts = np.fromiter((r.start_row for r in self.ranges), dtype=np.uint64, count=len(self.ranges))
             counts = np.fromiter((r.row_count for r in self.ranges), dtype=np.uint64, count=len(self.ranges))
-            cached = (key, starts, counts)
+            cached = (key, starts, counts, (starts.ctypes.data, counts.ctypes.data, len(self.ranges)))
             self._arrays = cached
-        return cached[1], cached[2]
+        return cached
 
 
 @dataclass
@@ -403,20 +410,22 @@ class Engine:
             rows = n_rows if n_rows is not None else _rows_of(dataset, p)
             src.first_row = first_row
             src.n_rows = rows
-        R = len(plan.partition.ranges)
-        starts, counts = plan.partition.arrays()
-        out = SuffStats.empty(schema, plan.precision)
+        a_starts, a_counts, R = plan.partition.addresses()
+        # one ctypes buffer [sums | cross] viewed by numpy: no per-call pointer objects
+        E = p + p * (p + 1) // 2
+        res = (ctypes.c_double * E)()
+        a_res = ctypes.addressof(res)
         n = ctypes.c_uint64()
         err = N.Error()
         tm = N.Timings()
-        dp = ctypes.POINTER(ctypes.c_double)
-        st = self._lib.sstat_cuda_dataset(self._ctx, ctypes.byref(src), p, starts.ctypes.data, counts.ctypes.data, R,
-                                          int(plan.precision), flags, ctypes.byref(n), out.sums.ctypes.data_as(dp),
-                                          out.cross.ctypes.data_as(dp), ctypes.byref(tm), ctypes.byref(err))
+        st = self._lib.sstat_cuda_dataset(self._ctx, ctypes.byref(src), p, a_starts, a_counts, R,
+                                          int(plan.precision), flags, ctypes.byref(n), a_res, a_res + 8 * p,
+                                          ctypes.byref(tm), ctypes.byref(err))
         del keep
         if st != N.OK:
             _raise(st, err, in_dataset=True)
-        out.n = n.value
+        flat = np.frombuffer(res, dtype=np.float64)
+        out = SuffStats(n.value, flat[:p], flat[p:], schema, PrecisionMode(plan.precision))
         if timings is not None:
             timings.read_seconds = tm.h2d_seconds
             timings.work_seconds = tm.kernel_seconds + tm.fold_seconds
