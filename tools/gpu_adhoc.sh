@@ -1,4 +1,6 @@
-timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
-timeout 300 python tools/step_profile.py 1e6 9 > gpurun_out/step_c1.log 2>&1
-timeout 600 python bench.py --config c1 --no-cpu --no-e2e --no-next > gpurun_out/bench_c1q.log 2>&1
-timeout 600 python bench.py --no-cpu --no-e2e --no-next > gpurun_out/bench_c2q.log 2>&1
+export SWEEP_P=96,128,192,256,384,512
+for v in "SSTAT_WIDEP_PF=0" "SSTAT_WIDEP_PF=4" "SSTAT_WIDEP_PF=8" "SSTAT_WIDEP_PF=16" "SSTAT_WIDEP_PF=32"; do
+  echo "== $v" >> gpurun_out/pf.log
+  env $v SSTAT_SPLITP=0 timeout 300 python tools/p_sweep.py 1.6e10 >> gpurun_out/pf.log 2>&1
+done
+timeout 900 python bench.py --config c5 --no-cpu --no-e2e --no-next > gpurun_out/bench_c5_pf.log 2>&1
