@@ -282,10 +282,12 @@ __device__ __forceinline__ void consume_stage(double (&acc)[R * R][2], double (&
 // SROWS = rows per ring stage (compile-time, so a stage is one straight-line program with
 // the next k-step's fragment loads issued under the current k-step's DMMAs).  Launched with
 // cluster dimension geo.csize (1 = no cluster).
-template <int SROWS, int R>
-__global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t tile_rows) {
+// Warps [0, consumers) consume; warp `consumers` is the producer; any further warps (the
+// rest of the producer warpgroup of k_widep_wg) follow the producer's unit sequence without
+// issuing anything, so every collective (barrier.sync 1, barrier.cluster) sees all threads.
+template <int SROWS, int R, bool WG>
+__device__ __forceinline__ void widep_body(const TileJob& job, const WideGeom& geo, uint32_t tile_rows, double* sm) {
     // ring x (SROWS x pitch) | kSlack doubles | full[ring] | empty[ring]
-    extern __shared__ __align__(128) double sm[];
     const uint32_t p = geo.p, pitch = geo.pitch, nb = geo.nb, ring = geo.ring, K = geo.csize;
     const uint32_t slot_elems = SROWS * pitch;
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + ring * slot_elems + kSlack);
@@ -339,11 +341,13 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
     if (K > 1) cluster_sync_all(); else __syncthreads();
 
     uint32_t slot = 0, ph = 0;  // ring position, advanced once per stage
-    if (warp == (int)consumers) {
+    if (warp >= (int)consumers) {
         // ---------------- producer ----------------
+        if (WG) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
         const uint16_t mask = (uint16_t)((1u << K) - 1);
         uint64_t u = u_first;
         for (uint32_t it = 0; next_unit(u, it); ++it) {
+            if (warp != (int)consumers) continue;  // idle warps of the producer warpgroup
             const UnitInfo ui = unit_info(job, geo, tile_rows, unit_tile(u));
             const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
             const double* crow = job.shift != nullptr ? job.shift + (uint64_t)ui.r * p : nullptr;
@@ -405,6 +409,7 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
         }
     } else {
         // ---------------- consumers ----------------
+        if (WG) asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n" ::: "memory");
         const int g = lane >> 2, kk = lane & 3;
         const uint64_t E = partial_len(p);
         uint64_t u = u_first;
@@ -477,6 +482,24 @@ __global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t til
     if (K > 1) cluster_sync_all();
 }
 
+template <int SROWS, int R>
+__global__ void __maxnreg__(168) k_widep(TileJob job, WideGeom geo, uint32_t tile_rows) {
+    extern __shared__ __align__(128) double sm[];
+    widep_body<SROWS, R, false>(job, geo, tile_rows, sm);
+}
+
+// Three consumer warpgroups (12 warps, three per SM sub-partition) + one producer warpgroup
+// in a 512-thread CTA, one CTA per SM: launched at 128 registers per thread, the producer
+// warpgroup hands registers to the consumers (setmaxnreg: 3 x 152 + 56 = 512 per
+// sub-partition lane), which a dedicated producer warp could not do (a 13th warp would put
+// four warps on one sub-partition and cap every warp at 128 registers).
+constexpr uint32_t kWgConsumers = 12;
+template <int SROWS, int R>
+__global__ void __launch_bounds__(512, 1) k_widep_wg(TileJob job, WideGeom geo, uint32_t tile_rows) {
+    extern __shared__ __align__(128) double sm[];
+    widep_body<SROWS, R, true>(job, geo, tile_rows, sm);
+}
+
 // Rectangles (I <= J) of the nr x nr rectangle grid, dealt to n_groups groups of
 // `consumers` warps (the last groups padded with idle warps).
 std::vector<uint32_t> make_items(uint32_t nr, uint32_t consumers, uint32_t n_groups) {
@@ -496,6 +519,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // rectangle table kept on the device for the life of the process.
 struct Plan {
     int device = -1;
+    bool wg = false;  // k_widep_wg (12 consumer warps) instead of k_widep
     uint32_t p = 0, srows = 0, R = 0, grid_cap = 0;  // grid_cap = clusters in flight
     size_t smem = 0;
     WideGeom geo{};
@@ -512,9 +536,10 @@ cudaStream_t g_side[64] = {};  // per-device side stream for the spare plan
 std::vector<Plan> g_plans;
 
 template <int SROWS, int R>
-cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster = false) {
-    auto kern = k_widep<SROWS, R>;
-    const int threads = (int)(geo.consumers + 1) * 32;
+cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster, bool wg) {
+    auto kern = wg ? k_widep_wg<SROWS, R> : k_widep<SROWS, R>;
+    if (wg) geo.consumers = kWgConsumers;
+    const int threads = wg ? 512 : (int)(geo.consumers + 1) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     // the opt-in limit only caps what a launch may request; set it once to the maximum so
@@ -528,10 +553,10 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster 
     // deepest ring (2..4 stages) that keeps the target CTAs per SM (2 for 4-warp groups, so
     // two groups share an SM's four DMMA units; 1 for 8-warp groups)
     // smaller rectangles need fewer registers: three 4-warp CTAs per SM
-    const int want = (int)env_u32("SSTAT_WIDEP_PERSM", geo.consumers == 4 ? (R == 4 ? 2 : 3) : 1);
+    const int want = wg ? 1 : (int)env_u32("SSTAT_WIDEP_PERSM", geo.consumers == 4 ? (R == 4 ? 2 : 3) : 1);
     size_t smem = 0;
     int per_sm = 0;
-    for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", 4); ring >= 2; --ring) {
+    for (uint32_t ring = env_u32("SSTAT_WIDEP_RING", wg ? 12 : 4); ring >= 2; --ring) {
         geo.ring = ring;
         smem = sizeof(double) * (ring * SROWS * geo.pitch + kSlack) + 2 * ring * sizeof(uint64_t);
         if (smem > max_dyn) continue;
@@ -606,6 +631,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster 
     if (e != cudaSuccess) return e;
     best.items = d_items;
     out.device = device;
+    out.wg = wg;
     out.p = geo.p;
     out.srows = SROWS;
     out.R = R;
@@ -614,8 +640,8 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster 
     out.smem = smem;
     out.geo = best;
     if (getenv("SSTAT_DEBUG"))
-        fprintf(stderr, "k_widep<%d,%d>: p=%u C=%u groups=%u/%u cluster=%u x %u ring=%u smem=%zu per_sm=%d clusters=%u\n",
-                SROWS, R, geo.p, best.consumers, groups, best.n_groups, best.csize, best.cpt, best.ring, smem, per_sm,
+        fprintf(stderr, "k_widep%s<%d,%d>: p=%u C=%u groups=%u/%u cluster=%u x %u ring=%u smem=%zu per_sm=%d clusters=%u\n",
+                wg ? "_wg" : "", SROWS, R, geo.p, best.consumers, groups, best.n_groups, best.csize, best.cpt, best.ring, smem, per_sm,
                 best_clusters);
     return cudaSuccess;
 }
@@ -630,28 +656,30 @@ cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream)
     attr[0].val.clusterDim.x = pl.geo.csize;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3((pl.geo.consumers + 1) * 32);
+    cfg.blockDim = dim3(pl.wg ? 512 : (pl.geo.consumers + 1) * 32);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const uint64_t units = tiles * pl.geo.cpt;
     cfg.gridDim = dim3((unsigned)(std::min<uint64_t>(units, pl.grid_cap) * pl.geo.csize));
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_widep<SROWS, R>, job, pl.geo, widep_tile_rows(pl.geo.p));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, pl.wg ? k_widep_wg<SROWS, R> : k_widep<SROWS, R>, job, pl.geo,
+                                       widep_tile_rows(pl.geo.p));
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 template <int SROWS>
-cudaError_t make_plan_r(int device, const WideGeom& geo, Plan& out, bool force_nocluster) {
-    return geo.R == 2 ? make_plan<SROWS, 2>(device, geo, out, force_nocluster)
-           : geo.R == 3 ? make_plan<SROWS, 3>(device, geo, out, force_nocluster)
-                        : make_plan<SROWS, 4>(device, geo, out, force_nocluster);
+cudaError_t make_plan_r(int device, const WideGeom& geo, Plan& out, bool force_nocluster, bool wg) {
+    return geo.R == 2 ? make_plan<SROWS, 2>(device, geo, out, force_nocluster, wg)
+           : geo.R == 3 ? make_plan<SROWS, 3>(device, geo, out, force_nocluster, wg)
+                        : make_plan<SROWS, 4>(device, geo, out, force_nocluster, wg);
 }
-cudaError_t make_plan_any(int device, const WideGeom& geo, uint32_t srows, Plan& out, bool force_nocluster = false) {
-    return srows == 16 ? make_plan_r<16>(device, geo, out, force_nocluster)
-           : srows == 8 ? make_plan_r<8>(device, geo, out, force_nocluster)
-                        : make_plan_r<4>(device, geo, out, force_nocluster);
+cudaError_t make_plan_any(int device, const WideGeom& geo, uint32_t srows, Plan& out, bool force_nocluster,
+                          bool wg) {
+    return srows == 16 ? make_plan_r<16>(device, geo, out, force_nocluster, wg)
+           : srows == 8 ? make_plan_r<8>(device, geo, out, force_nocluster, wg)
+                        : make_plan_r<4>(device, geo, out, force_nocluster, wg);
 }
 template <int SROWS>
 cudaError_t launch_plan_r(const TileJob& job, const Plan& pl, cudaStream_t stream) {
@@ -677,15 +705,76 @@ uint32_t choose_r(uint32_t nb, uint32_t consumers) {
         // 2x2 rectangles load one fragment per DMMA and need twice the groups per tile: measured
         // 15-25 % below this model from p = 136 on (profiles/r01_p_sweep.log), hence the 1.25
         // (not at nb <= 12, where they measured best)
-        const double cost = slots * (R * R + R / 4.0) / (nb * (nb + 1) / 2.0) * (R == 2 && nb > 12 ? 1.25 : 1.0);
+        // 3x3 rectangles: 9 DMMA per 6 fragments, measured ~15 % below the model where the
+        // costs are close (p = 200, 296, 352: profiles/r01_k2_wg_sweep.log), hence 1.15
+        const double pen = R == 2 && nb > 12 ? 1.25 : R == 3 ? 1.15 : 1.0;
+        const double cost = slots * (R * R + R / 4.0) / (nb * (nb + 1) / 2.0) * pen;
         if (best_cost == 0 || cost < 0.97 * best_cost) best = R, best_cost = cost;
     }
     return best;
 }
 
+// Share of the consumer warp slots (groups x warps, idle padding included) that own a rectangle.
+double plan_efficiency(const Plan& pl) {
+    const double items = pl.geo.nr * (pl.geo.nr + 1) / 2.0;
+    return items / ((double)pl.geo.n_groups * pl.geo.consumers);
+}
+void free_plan(const Plan& pl) {
+    cudaFree(const_cast<uint32_t*>(pl.geo.items));
+    if (pl.has_spare) cudaFree(const_cast<uint32_t*>(pl.spare_geo.items));
+}
+
+// The launch geometry for width p with the 4/8-warp kernel (wg = false) or k_widep_wg, plus the
+// cluster-less side plan for the CTA slots its cluster placement leaves idle.
+cudaError_t build_plan(int device, uint32_t p, uint32_t srows, bool wg, Plan& pl) {
+    WideGeom geo{};
+    geo.p = p;
+    geo.nb = (p + 7) / 8;
+    geo.R = env_u32("SSTAT_WIDEP_R", choose_r(geo.nb, wg ? kWgConsumers : 4));
+    if (geo.R < 2 || geo.R > 4) geo.R = 4;
+    geo.nr = (geo.nb + geo.R - 1) / geo.R;
+    // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank
+    // groups, so each half-warp fragment read is one conflict-free wavefront
+    // (odd p: unpadded, the stage is copied as row pairs; see k_widep)
+    geo.pitch = p % 2 ? p : ((p + 15) / 16) * 16 + 4;
+    // 4-warp groups (two CTAs per SM) leave at most 3 idle rectangles per tile, 8-warp
+    // groups up to 7 but re-read less; the multicast makes the extra groups cheap
+    // (measured: 4-warp groups win up to p = 512, +5 % at 384 and +14 % at 512; even at 1024)
+    const uint32_t items = geo.nr * (geo.nr + 1) / 2;
+    geo.consumers = std::min<uint32_t>(12, std::max<uint32_t>(1, env_u32("SSTAT_WIDEP_CONSUMERS", items <= 300 ? 4 : 8)));
+    // 12-consumer-warp CTAs: registers cap them at 8-row stages for 4x4 rectangles
+    if (wg && geo.R == 4 && srows > 8) srows = 8;
+    cudaError_t e = make_plan_any(device, geo, srows, pl, false, wg);
+    if (e != cudaSuccess) return e;
+    const uint64_t slots = (uint64_t)sms_of(device) * pl.resident;
+    const uint64_t used = (uint64_t)pl.grid_cap * pl.geo.csize;
+    // CTA slots the cluster placement leaves idle get a cluster-less launch (>= 4 % of
+    // the slots, whole-tile clusters only)
+    if (pl.geo.csize > 1 && pl.geo.cpt == 1 && slots > used && 25 * (slots - used) >= slots) {
+        Plan ps;
+        WideGeom g2 = geo;
+        g2.consumers = pl.geo.consumers;
+        e = make_plan_any(device, g2, srows, ps, true, wg);
+        if (e != cudaSuccess) return e;
+        if (!g_side[device]) {
+            e = cudaStreamCreateWithFlags(&g_side[device], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return e;
+        }
+        pl.has_spare = true;
+        pl.spare_ctas = (uint32_t)(slots - used);
+        pl.spare_smem = ps.smem;
+        pl.spare_geo = ps.geo;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace
 
 uint32_t widep_tile_rows(uint32_t) { return 32768; }
+
+namespace {
+cudaError_t launch_forked(const TileJob& job, const Plan& pl, int device, cudaStream_t stream, uint32_t* kernels);
+}
 
 cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t* kernels) {
     if (kernels) *kernels = 1;
@@ -696,9 +785,10 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
     if (e != cudaSuccess) return e;
     // stage height: 16 rows up to p = 256, then 8, then 4 (a stage stays ~33 KB)
     uint32_t srows = p <= 256 ? 16 : p <= 512 ? 8 : 4;
-    if (p <= 256 && env_u32("SSTAT_WIDEP_SROWS", 16) == 8) srows = 8;
+    if (const uint32_t e = env_u32("SSTAT_WIDEP_SROWS", 0)) srows = e >= 16 ? 16 : e >= 8 ? 8 : 4;
     const bool tuned = getenv("SSTAT_WIDEP_CONSUMERS") || getenv("SSTAT_WIDEP_NOCLUSTER") ||
-                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS") || getenv("SSTAT_WIDEP_PERSM") || getenv("SSTAT_WIDEP_R");
+                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS") || getenv("SSTAT_WIDEP_PERSM") || getenv("SSTAT_WIDEP_R") ||
+                       getenv("SSTAT_WIDEP_WG");
     Plan pl;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -707,47 +797,43 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
             for (const Plan& q : g_plans)
                 if (q.device == device && q.p == p) pl = q, found = true;
         if (!found) {
-            WideGeom geo{};
-            geo.p = p;
-            geo.nb = (p + 7) / 8;
-            geo.R = env_u32("SSTAT_WIDEP_R", choose_r(geo.nb, 4));
-            if (geo.R < 2 || geo.R > 4) geo.R = 4;
-            geo.nr = (geo.nb + geo.R - 1) / geo.R;
-            // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank
-            // groups, so each half-warp fragment read is one conflict-free wavefront
-            // (odd p: unpadded, the stage is copied as row pairs; see k_widep)
-            geo.pitch = p % 2 ? p : ((p + 15) / 16) * 16 + 4;
-            // 4-warp groups (two CTAs per SM) leave at most 3 idle rectangles per tile, 8-warp
-            // groups up to 7 but re-read less; the multicast makes the extra groups cheap
-            const uint32_t items = geo.nr * (geo.nr + 1) / 2;
-            // (measured: 4-warp groups win up to p = 512, +5 % at 384 and +14 % at 512; even at 1024)
-            geo.consumers = env_u32("SSTAT_WIDEP_CONSUMERS", items <= 300 ? 4 : 8) == 4 ? 4 : 8;
-            e = make_plan_any(device, geo, srows, pl);
-            if (e != cudaSuccess) return e;
-            const uint64_t slots = (uint64_t)sms_of(device) * pl.resident;
-            const uint64_t used = (uint64_t)pl.grid_cap * pl.geo.csize;
-            // CTA slots the cluster placement leaves idle get a cluster-less launch (>= 4 % of
-            // the slots, whole-tile clusters only)
-            if (pl.geo.csize > 1 && pl.geo.cpt == 1 && slots > used && 25 * (slots - used) >= slots) {
-                Plan ps;
-                WideGeom g2 = geo;
-                g2.consumers = pl.geo.consumers;
-                e = make_plan_any(device, g2, srows, ps, true);
-                if (e != cudaSuccess) return e;
-                if (!g_side[device]) {
-                    e = cudaStreamCreateWithFlags(&g_side[device], cudaStreamNonBlocking);
-                    if (e != cudaSuccess) return e;
+            // the 12-consumer-warp kernel (three warps per SM sub-partition instead of two)
+            // unless its 12-warp groups pad the rectangle grid more than 6 % worse than the
+            // 4-warp groups do (measured, profiles/r01_k2_wg_sweep.log: +4 % at p = 256,
+            // +8 % at 416-448, +18-22 % at 640-1024; worse below p = 136 and at p = 168, 384)
+            const char* wg_env = getenv("SSTAT_WIDEP_WG");
+            const uint32_t nb = (p + 7) / 8;
+            if (wg_env) {
+                e = build_plan(device, p, srows, atoi(wg_env) != 0, pl);
+            } else if (nb <= 16) {
+                e = build_plan(device, p, srows, false, pl);
+            } else {
+                Plan pc, pw;
+                e = build_plan(device, p, srows, false, pc);
+                if (e == cudaSuccess) e = build_plan(device, p, srows, true, pw);
+                if (e == cudaSuccess) {
+                    const bool use_wg = plan_efficiency(pw) >= 0.94 * plan_efficiency(pc);
+                    pl = use_wg ? pw : pc;
+                    free_plan(use_wg ? pc : pw);
+                    if (getenv("SSTAT_DEBUG"))
+                        fprintf(stderr, "k_widep: p=%u efficiency 4-warp %.3f, 12-warp %.3f -> %s\n", p,
+                                plan_efficiency(pc), plan_efficiency(pw), use_wg ? "k_widep_wg" : "k_widep");
                 }
-                pl.has_spare = true;
-                pl.spare_ctas = (uint32_t)(slots - used);
-                pl.spare_smem = ps.smem;
-                pl.spare_geo = ps.geo;
             }
+            if (e != cudaSuccess) return e;
             if (!tuned) g_plans.push_back(pl);
         }
     }
+    e = launch_forked(job, pl, device, stream, kernels);
+    if (tuned) free_plan(pl);  // experiment plans are not cached (cudaFree waits for the launches)
+    return e;
+}
+
+namespace {
+cudaError_t launch_forked(const TileJob& job, const Plan& pl, int device, cudaStream_t stream, uint32_t* kernels) {
     if (!pl.has_spare || !job.claim || job.tile_end - job.tile_begin < 2 || env_u32("SSTAT_WIDEP_SPARE", 1) == 0)
         return launch_plan_any(job, pl, stream);
+    cudaError_t e;
     // fork: the clustered plan on `stream` and the cluster-less plan on the side stream claim
     // tiles / units dynamically from one word (claim_unit); if the side launch cannot run
     // alongside, the clustered one simply takes every tile.  Join before returning.
@@ -776,5 +862,6 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
     cudaEventDestroy(join);
     return e != cudaSuccess ? e : e2;
 }
+}  // namespace
 
 }  // namespace sstat_b200

@@ -554,7 +554,8 @@ def test_widest_fast_path_and_limit(engine, oracle):
 def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     """K2's result is a fixed function of the tile: 4- or 8-warp groups, with or without the
     cluster multicast, with or without the cluster-less side launch claiming tiles
-    dynamically, and 2-, 3- or 4-block rectangles give the same bits."""
+    dynamically, 2-, 3- or 4-block rectangles, and the 12-consumer-warp k_widep_wg give the
+    same bits."""
     torch = torch_mod()
     monkeypatch.setenv("SSTAT_SPLITP", "0")  # K2 itself at every p (K1w takes 64 < p <= 128 by default)
     n = 100003 if p <= 256 else 40001
@@ -563,7 +564,9 @@ def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     pl = plan(n, 30011)
     base = engine.dataset_suffstats(D, schema(p), pl)
     for env in ({"SSTAT_WIDEP_CONSUMERS": "8"}, {"SSTAT_WIDEP_CONSUMERS": "4"}, {"SSTAT_WIDEP_NOCLUSTER": "1"},
-                {"SSTAT_WIDEP_SPARE": "0"}, {"SSTAT_WIDEP_R": "2"}, {"SSTAT_WIDEP_R": "3"}, {"SSTAT_WIDEP_R": "4"}):
+                {"SSTAT_WIDEP_SPARE": "0"}, {"SSTAT_WIDEP_R": "2"}, {"SSTAT_WIDEP_R": "3"}, {"SSTAT_WIDEP_R": "4"},
+                {"SSTAT_WIDEP_WG": "1"}, {"SSTAT_WIDEP_WG": "1", "SSTAT_WIDEP_R": "3"},
+                {"SSTAT_WIDEP_WG": "1", "SSTAT_WIDEP_SPARE": "0"}, {"SSTAT_WIDEP_WG": "1", "SSTAT_WIDEP_NOCLUSTER": "1"}):
         with monkeypatch.context() as m:
             for k, v in env.items():
                 m.setenv(k, v)
