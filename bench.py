@@ -336,10 +336,13 @@ def run_ours(args):
             "column_sum": {"value": n_global / t_cs, "unit": "rows/s", "ms_per_step": t_cs * 1e3, "column": 0,
                            "what": "column_sum (reduce.cpp:32-88): FP64 sum + exact 128-bit integer sum of one column",
                            "column_gb_per_s": local_rows * 8 / t_cs / 1e9,
-                           "row_gb_per_s": local_rows * p * 8 / t_cs / 1e9,
-                           "note": "row-major rows: the memory system moves each row's whole 128-B line for one "
-                                   "8-B column (ncu: 4 L2 sectors per row, DRAM read = all 8p bytes), so the "
-                                   "bound is the row bytes at HBM bandwidth"},
+                           # bytes the memory system must move per row for one 8-B column: the
+                           # whole row while it fits one 128-B line (ncu at C2: 4 L2 sectors per
+                           # row, DRAM read = all 8p bytes), else at least one 32-B sector
+                           "moved_gb_per_s": local_rows * (8 * p if 8 * p <= 128 else 32) / t_cs / 1e9,
+                           "note": "row-major rows: one 8-B column costs the whole row up to 128-B rows "
+                                   "(C2: the bound is the row bytes at HBM bandwidth) and at least a 32-B "
+                                   "sector per row beyond"},
             "comoments": {"value": n_global / t_cm, "unit": "rows/s", "ms_per_step": t_cm * 1e3,
                           "what": "run_reduction(accumulate_comoments, merge_comoments) (suffstats.cpp:107-159)",
                           "gb_per_s": local_rows * p * 8 / t_cm / 1e9},

@@ -4,7 +4,8 @@ timeout 1200 python -m pytest tests -q -m gpu 2>&1 | tail -5 > gpurun_out/pytest
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_reference.log 2>&1
-for c in c1 c4 c5; do timeout 900 python bench.py --steps 5 --warmup 3 --config $c > gpurun_out/bench_$c.log 2>&1; done
+timeout 600 python bench.py --steps 50 --warmup 5 --config c1 > gpurun_out/bench_c1.log 2>&1
+for c in c4 c5; do timeout 900 python bench.py --steps 5 --warmup 3 --config $c > gpurun_out/bench_$c.log 2>&1; done
 timeout 900 python bench.py --impl reference --config c5 --steps 2 --warmup 1 > gpurun_out/bench_reference_c5.log 2>&1
 timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-next > gpurun_out/plain.log 2>&1 &&
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \

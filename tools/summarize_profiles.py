@@ -68,7 +68,7 @@ if __name__ == "__main__":
     with open(f"profiles/{tag}_launches.md", "w") as f:
         f.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none, cold & serialised)\n\n")
         f.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py "
-                "--steps 2 --warmup 3 --no-e2e --no-cpu`\n\n")
+                "--steps 2 --warmup 3 --no-e2e --no-cpu --no-next`\n\n")
         f.write(launches(lc) + "\n")
     with open(f"profiles/{tag}_k1_full.md", "w") as f:
         f.write(f"# {tag}: ncu --set full of the accumulate kernel (one launch, C2 1e8 x 16)\n\n")
