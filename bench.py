@@ -126,6 +126,18 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def cpu_model() -> str:
+    """The host CPU model string (report it beside the CPU timing)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_rows_per_s(steps: int, warmup: int, config: str = "c2"):
     """The reference's own dataset_suffstats (oracle/_ref) on a 2.56 GB SSTATBIN sample of the
     config's workload (same generator, same p, chunk 2^20), all host threads.  Returns
@@ -195,7 +207,7 @@ def run_reference_arm(args):
                                f"{args.config.upper()} (p={p}, chunk_rows 2^20, SSTATBIN in page cache)",
                    "p": p, "sample_rows": sample},
         "gb_per_s": v * 8 * p / 1e9,
-        "cpu_baseline": {"value": v, "unit": "rows/s", "cores": cores, "kind": "reference",
+        "cpu_baseline": {"value": v, "unit": "rows/s", "cores": cores, "kind": "reference", "cpu": cpu_model(),
                          "sample": f"{sample} rows x {p} of the {args.config.upper()} generator, one "
                                    f"dataset_suffstats pass per step, {cores} worker threads; "
                                    f"last step read {split[0]:.2f} s / work {split[1]:.2f} s (summed over workers)"},
@@ -388,7 +400,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rates, cores, split, sample = cpu_reference_rows_per_s(steps=3, warmup=1, config=args.config)
-        cpu = {"value": statistics.median(rates), "unit": "rows/s", "cores": cores, "kind": "reference",
+        cpu = {"value": statistics.median(rates), "unit": "rows/s", "cores": cores, "kind": "reference", "cpu": cpu_model(),
                "sample": f"reference dataset_suffstats (oracle/_ref) over {sample} rows x {p} of the same "
                          f"generator, chunk_rows 2^20, {cores} worker threads, median of 3 passes"}
 
