@@ -653,8 +653,10 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     };
 
     // ---- K1 on a resident shard, one GPU: the whole pass as one replayed CUDA graph ----
-    // (launch-bound for small shards: four kernels, five events and the read-back become one
-    // cudaGraphLaunch; captured on a private stream, keyed by every input the launches bake in)
+    // (launch-bound for small shards: four kernels, three events and the read-back become one
+    // cudaGraphLaunch; captured on a private stream, keyed by every input the launches bake in.
+    // Each external event node costs ~5-7 us of replay: the graph times K1 and the two folds
+    // together — five events measured 14 us slower per call at C1 and C2)
     const bool graphable = src->kind == SSTAT_SRC_DEVICE && world == 1 && P.mode == Mode::Dataset && !refexact &&
                            !wide && L > 0 && nt > 0 && !getenv("SSTAT_NO_GRAPH");
     if (graphable) {
@@ -694,8 +696,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                 CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
                 CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
                                            (uint32_t)L, p, P.r0, rank_buf, d_flags, cs));
-                CUDA_TRY(cudaEventRecordWithFlags(c->ev[2], cs, cudaEventRecordExternal));
-                CUDA_TRY(cudaEventRecordWithFlags(c->ev[3], cs, cudaEventRecordExternal));
+
                 CUDA_TRY(launch_final_fold(rank_buf, rank_stride, P.R, 1, p, 0u, false, c->d_result.as<double>(), cs));
                 CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
                 CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + kHdr) * 8, cudaMemcpyDeviceToHost, cs));
@@ -930,7 +931,14 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     }
     c->flags_clean = !any_flag;
     std::memcpy(result_host, hres, E * 8);
-    if (tm) {
+    if (tm && graphable) {  // the graph records three events: K1, then both folds together
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+        tm->kernel_seconds += ms * 1e-3;
+        cudaEventElapsedTime(&ms, c->ev[1], c->ev[4]);
+        tm->fold_seconds += ms * 1e-3;
+        tm->n_local_ranges = (uint32_t)L;
+    } else if (tm) {
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
         tm->kernel_seconds += ms * 1e-3;
