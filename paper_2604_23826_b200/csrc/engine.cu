@@ -576,6 +576,14 @@ uint64_t* upload_meta(sstat_cuda_ctx* c, Plan& P, uint64_t TR, cudaStream_t s) {
     return d_starts;
 }
 
+// Every range of [starts, starts + n) begins on a 16-byte boundary of the rows at `base`.
+bool rows_aligned16(const double* base, uint64_t base_row, const uint64_t* starts, uint64_t n, uint32_t p) {
+    if (reinterpret_cast<uintptr_t>(base) % 16) return false;
+    for (uint64_t i = 0; i < n; ++i)
+        if (((starts[i] - base_row) * p) % 2) return false;
+    return true;
+}
+
 // The engine proper.  Returns the all-rank outcome; throws Fail.
 void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
          sstat_cuda_timings* tm) {
@@ -729,7 +737,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         const uint64_t base_row = src->first_row;
         if (refexact) {
             CUDA_TRY(launch_refexact(base, base_row, d_starts, d_counts, (uint32_t)L, p, P.precision, P.r0, rank_buf,
-                                     rank_buf + kHdr, d_flags, s));
+                                     rank_buf + kHdr, d_flags, rows_aligned16(base, base_row, P.starts + P.r0, L, p), s));
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
             if (tm) tm->kernel_launches += 1;
         } else {
@@ -793,7 +801,9 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                               // ranges [u0, u1) of this chunk → partial slots u0 .. u1-1
                               CUDA_TRY(launch_refexact(base, base_row, d_starts + u0, d_counts + u0, (uint32_t)(u1 - u0),
                                                        p, P.precision, P.r0 + u0, rank_buf, rank_buf + kHdr + u0 * E,
-                                                       d_flags + u0, s));
+                                                       d_flags + u0,
+                                                       rows_aligned16(base, base_row, P.starts + P.r0 + u0, u1 - u0, p),
+                                                       s));
                           },
                           tm);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));

@@ -229,6 +229,99 @@ __global__ void __launch_bounds__(128) k_refexact_staged(const double* __restric
     }
 }
 
+// The same chains with the chunks streamed by TMA: one thread issues each chunk (contiguous rows,
+// 16-byte aligned) as a single bulk copy into a kRefStages-deep shared-memory ring completing on
+// the slot's mbarrier, so up to kRefStages chunks are in flight per block instead of one; the
+// chains then run exactly as in k_refexact_staged (same operations, same order).
+constexpr uint32_t kRefStages = 4;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <typename Acc>
+__global__ void __launch_bounds__(128) k_refexact_tma(const double* __restrict__ base, uint64_t base_row,
+                                                      const uint64_t* __restrict__ range_start,
+                                                      const uint64_t* __restrict__ range_count, uint32_t p,
+                                                      uint64_t first_range, double* hdr, double* out, uint32_t* flags,
+                                                      uint32_t ch) {
+    extern __shared__ __align__(128) double stage[];  // [kRefStages][ch * p] | full[kRefStages]
+    const uint32_t chunk_elems = ch * p;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage + kRefStages * chunk_elems);
+    const uint64_t E = partial_len(p);
+    const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint32_t r = blockIdx.y;
+    const bool active = e < E;
+    const bool is_sum = e < p;
+    uint32_t j = active ? (uint32_t)e : 0, k = j;
+    if (active && !is_sum) unpack_index(p, (uint32_t)(e - p), j, k);
+    const double* rows = base + (range_start[r] - base_row) * p;
+    const uint64_t n = range_count[r];
+    const uint64_t n_chunks = (n + ch - 1) / ch;
+    auto issue = [&](uint64_t c) {  // thread 0
+        const uint64_t row0 = c * ch;
+        const uint32_t elems = (uint32_t)((n - row0 < (uint64_t)ch ? n - row0 : ch) * p);
+        const uint32_t bulk = (elems & ~1u) * 8;  // a whole number of 16-byte units
+        double* dst = stage + (c % kRefStages) * chunk_elems;
+        const double* src = rows + row0 * p;
+        uint64_t* bar = &full[c % kRefStages];
+        if (elems & 1) dst[elems - 1] = src[elems - 1];  // odd tail double: a plain store, before the arrive
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bulk)
+                     : "memory");
+        if (bulk)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_addr(dst)),
+                "l"(src), "r"(bulk), "r"(smem_addr(bar))
+                : "memory");
+    };
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < kRefStages; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(&full[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (uint64_t c = 0; c < n_chunks && c < kRefStages; ++c) issue(c);
+    }
+    __syncthreads();
+    Acc acc = Acc(0);
+    for (uint64_t c = 0; c < n_chunks; ++c) {
+        const uint32_t parity = (uint32_t)((c / kRefStages) & 1);
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@!P1 bra WAIT_%=;\n"
+            "}\n" ::"r"(smem_addr(&full[c % kRefStages])),
+            "r"(parity)
+            : "memory");
+        const double* x = stage + (c % kRefStages) * chunk_elems;
+        const uint32_t cnt = (uint32_t)(n - c * ch < (uint64_t)ch ? n - c * ch : ch);
+        if (active) {
+            uint32_t i = 0;
+            for (; i + 8 <= cnt; i += 8) {
+                double xj[8], xk[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    xj[u] = x[(i + u) * p + j];
+                    xk[u] = x[(i + u) * p + k];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    acc = is_sum ? add_rn(acc, cvt<Acc>(xj[u])) : add_rn(acc, mul_rn(cvt<Acc>(xj[u]), cvt<Acc>(xk[u])));
+            }
+            for (; i < cnt; ++i) {
+                const double a = x[i * p + j], b = x[i * p + k];
+                acc = is_sum ? add_rn(acc, cvt<Acc>(a)) : add_rn(acc, mul_rn(cvt<Acc>(a), cvt<Acc>(b)));
+            }
+        }
+        __syncthreads();  // every chain is done with the slot: refill it
+        if (threadIdx.x == 0 && c + kRefStages < n_chunks) issue(c + kRefStages);
+    }
+    if (!active) return;
+    const double v = (double)acc;
+    out[(uint64_t)r * E + e] = v;
+    if (is_sum && !finite64(v)) {
+        flags[r] = 1;
+        atomicMin(reinterpret_cast<ull*>(hdr), (ull)(first_range + r));
+    }
+}
+
 // ---- K5 generator: RowRng (rng.hpp:14-38) + Irwin-Hall Gaussians, IEEE ops in fixed order ----
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ULL;
@@ -320,10 +413,30 @@ cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t 
 
 cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_t* range_start,
                             const uint64_t* range_count, uint32_t n_ranges, uint32_t p, uint32_t precision,
-                            uint64_t first_range, double* hdr, double* out, uint32_t* flags, cudaStream_t stream) {
+                            uint64_t first_range, double* hdr, double* out, uint32_t* flags, bool rows_aligned16,
+                            cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
     const uint64_t E = partial_len(p);
     dim3 grid((unsigned)((E + 127) / 128), n_ranges);
+    // TMA ring when every range starts 16-byte aligned (the caller checks; chunks hold an even
+    // number of rows); SSTAT_REFEXACT_STAGED=1 keeps the cp.async kernel for comparison
+    if (rows_aligned16 && p <= 64 && !getenv("SSTAT_REFEXACT_STAGED")) {
+        uint32_t ch = (16384 / (8 * p)) & ~1u;  // 16 KB stages (three blocks per SM), an even number of rows
+        const size_t smem = (size_t)kRefStages * ch * p * sizeof(double) + kRefStages * sizeof(uint64_t);
+        cudaError_t e;
+        if (precision == 1) {
+            e = cudaFuncSetAttribute(k_refexact_tma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            k_refexact_tma<float><<<grid, 128, smem, stream>>>(base, base_row, range_start, range_count, p,
+                                                               first_range, hdr, out, flags, ch);
+        } else {
+            e = cudaFuncSetAttribute(k_refexact_tma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            k_refexact_tma<double><<<grid, 128, smem, stream>>>(base, base_row, range_start, range_count, p,
+                                                                first_range, hdr, out, flags, ch);
+        }
+        return cudaGetLastError();
+    }
     if (p <= 64) {  // rows staged through shared memory
         const uint32_t ch = std::min<uint32_t>(256, 6144 / p);
         const size_t smem = 2ull * ch * p * sizeof(double);

@@ -56,7 +56,8 @@ cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t 
 // Writes raw range partials out[r*E] and flags non-finite ranges (flags[r], hdr[0]).
 cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_t* range_start,
                             const uint64_t* range_count, uint32_t n_ranges, uint32_t p, uint32_t precision,
-                            uint64_t first_range, double* hdr, double* out, uint32_t* flags, cudaStream_t stream);
+                            uint64_t first_range, double* hdr, double* out, uint32_t* flags, bool rows_aligned16,
+                            cudaStream_t stream);
 
 // K5: synthetic rows [first_row, first_row + n_rows) (bit-identical to the oracle).
 cudaError_t launch_generate(double* dst, uint32_t kind, uint64_t seed, double mu, uint32_t n_int, uint64_t first_row,
