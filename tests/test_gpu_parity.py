@@ -550,7 +550,7 @@ def test_widest_fast_path_and_limit(engine, oracle):
     assert exact.n == wn and np.array_equal(bits(exact.cross), bits(wS)) and np.array_equal(bits(exact.sums), bits(ws))
 
 
-@pytest.mark.parametrize("p", [96, 256, 520])
+@pytest.mark.parametrize("p", [96, 256, 259, 520])
 def test_wide_p_schedule_invariant(engine, p, monkeypatch):
     """K2's result is a fixed function of the tile: 4- or 8-warp groups, with or without the
     cluster multicast, with or without the cluster-less side launch claiming tiles
