@@ -1,3 +1,2 @@
-timeout 300 python bench.py --steps 2 --warmup 3 --config c5 --no-cpu --no-e2e --no-next > gpurun_out/plain_c5b.log 2>&1 &&
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv \
-    python bench.py --steps 2 --warmup 3 --config c5 --no-cpu --no-e2e --no-next > gpurun_out/ncu_launch_c5.log 2>&1
+for i in 1 2; do timeout 1200 python -m pytest tests -q -m gpu 2>&1 | tail -3 >> gpurun_out/pytest_rep.log; done
+timeout 600 python tools/sanitize_cases.py > gpurun_out/san_plain.log 2>&1; echo "rc=$?" >> gpurun_out/san_plain.log
