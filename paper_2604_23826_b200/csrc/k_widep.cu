@@ -714,10 +714,11 @@ uint32_t choose_r(uint32_t nb, uint32_t consumers) {
     return best;
 }
 
-// Share of the consumer warp slots (groups x warps, idle padding included) that own a rectangle.
+// Share of the DMMA blocks a tile's warp slots compute (groups x warps x R^2, idle padding,
+// blocks past p and mirrored diagonal blocks included) that are upper-triangle blocks.
 double plan_efficiency(const Plan& pl) {
-    const double items = pl.geo.nr * (pl.geo.nr + 1) / 2.0;
-    return items / ((double)pl.geo.n_groups * pl.geo.consumers);
+    const double useful = pl.geo.nb * (pl.geo.nb + 1) / 2.0;
+    return useful / ((double)pl.geo.n_groups * pl.geo.consumers * pl.geo.R * pl.geo.R);
 }
 void free_plan(const Plan& pl) {
     cudaFree(const_cast<uint32_t*>(pl.geo.items));
@@ -798,9 +799,11 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
                 if (q.device == device && q.p == p) pl = q, found = true;
         if (!found) {
             // the 12-consumer-warp kernel (three warps per SM sub-partition instead of two)
-            // unless its 12-warp groups pad the rectangle grid more than 6 % worse than the
-            // 4-warp groups do (measured, profiles/r01_k2_wg_sweep.log: +4 % at p = 256,
-            // +8 % at 416-448, +18-22 % at 640-1024; worse below p = 136 and at p = 168, 384)
+            // unless its useful share of the computed DMMA blocks is more than 5 % below the
+            // 4-warp kernel's (measured, profiles/r01_k2_wg_sweep.log: +8-17 % at p = 136-144,
+            // +4 % at 256, +8 % at 416-448, +18-22 % at 640-1024; worse at p <= 128, at p = 168
+            // (its 4x4 rectangles: 60 % useful blocks against 92 % for 3x3 in 4-warp groups),
+            // 296 and 384)
             const char* wg_env = getenv("SSTAT_WIDEP_WG");
             const uint32_t nb = (p + 7) / 8;
             if (wg_env) {
@@ -812,7 +815,7 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
                 e = build_plan(device, p, srows, false, pc);
                 if (e == cudaSuccess) e = build_plan(device, p, srows, true, pw);
                 if (e == cudaSuccess) {
-                    const bool use_wg = plan_efficiency(pw) >= 0.94 * plan_efficiency(pc);
+                    const bool use_wg = plan_efficiency(pw) >= 0.95 * plan_efficiency(pc);
                     pl = use_wg ? pw : pc;
                     free_plan(use_wg ? pc : pw);
                     if (getenv("SSTAT_DEBUG"))

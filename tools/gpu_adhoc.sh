@@ -1,2 +1,1 @@
-for i in 1 2; do timeout 1200 python -m pytest tests -q -m gpu 2>&1 | tail -3 >> gpurun_out/pytest_rep.log; done
-timeout 600 python tools/sanitize_cases.py > gpurun_out/san_plain.log 2>&1; echo "rc=$?" >> gpurun_out/san_plain.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_next.py -q -x -k "wide or widest or misaligned or c5 or comoments" > gpurun_out/wide_pytest.log 2>&1
