@@ -705,9 +705,10 @@ uint32_t choose_r(uint32_t nb, uint32_t consumers) {
         // 2x2 rectangles load one fragment per DMMA and need twice the groups per tile: measured
         // 15-25 % below this model from p = 136 on (profiles/r01_p_sweep.log), hence the 1.25
         // (not at nb <= 12, where they measured best)
-        // 3x3 rectangles: 9 DMMA per 6 fragments, measured ~15 % below the model where the
-        // costs are close (p = 200, 296, 352: profiles/r01_k2_wg_sweep.log), hence 1.15
-        const double pen = R == 2 && nb > 12 ? 1.25 : R == 3 ? 1.15 : 1.0;
+        // 3x3 rectangles: 9 DMMA per 6 fragments, measured ~15 % below the model in 4-warp
+        // groups where the costs are close (p = 200, 296, 352) and ~5 % in 12-warp groups
+        // (p = 352 vs 296: profiles/r01_k2_wg_sweep.log)
+        const double pen = R == 2 && nb > 12 ? 1.25 : R == 3 ? (consumers >= 12 ? 1.05 : 1.15) : 1.0;
         const double cost = slots * (R * R + R / 4.0) / (nb * (nb + 1) / 2.0) * pen;
         if (best_cost == 0 || cost < 0.97 * best_cost) best = R, best_cost = cost;
     }

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_next.py -q -x -k "wide or widest or misaligned or c5 or comoments" > gpurun_out/wide_pytest.log 2>&1
+SWEEP_P=192,200,232,296,352,384 SSTAT_DEBUG=1 timeout 900 python tools/p_sweep.py 1.6e10 > gpurun_out/rule4.log 2>&1
