@@ -30,9 +30,13 @@
 // Launch geometry is chosen once per (device, p) from the occupancy calculator (make_plan).
 // When cluster placement leaves CTA slots idle, a second, cluster-less launch fills them on a
 // side stream and both claim work dynamically from one CAS-updated word (claim_unit).
+// k_widep_wg is the same body in one 512-thread CTA per SM: 12 consumer warps (three consumer
+// warpgroups) and a producer warpgroup that hands them registers (setmaxnreg); the plan for
+// each p builds both geometries and keeps the one wasting fewer DMMA blocks (launch_widep).
 // SSTAT_WIDEP_* environment variables override the choices for experiments and tests:
-// CONSUMERS (4 | 8), CLUSTER / MAXCLUSTER (K), NOCLUSTER, RING, SROWS (8 for p <= 256),
-// PERSM (CTAs per SM), SPARE=0 (no side launch), DEBUG (print the plan).
+// CONSUMERS (4 | 8), CLUSTER / MAXCLUSTER (K), NOCLUSTER, RING, SROWS (4 | 8 | 16), PERSM
+// (CTAs per SM), R (rectangle side), WG (0 | 1: the kernel), SPARE=0 (no side launch); and
+// SSTAT_DEBUG prints the plans.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -788,9 +792,12 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
     // stage height: 16 rows up to p = 256, then 8, then 4 (a stage stays ~33 KB)
     uint32_t srows = p <= 256 ? 16 : p <= 512 ? 8 : 4;
     if (const uint32_t e = env_u32("SSTAT_WIDEP_SROWS", 0)) srows = e >= 16 ? 16 : e >= 8 ? 8 : 4;
-    const bool tuned = getenv("SSTAT_WIDEP_CONSUMERS") || getenv("SSTAT_WIDEP_NOCLUSTER") ||
-                       getenv("SSTAT_WIDEP_MAXCLUSTER") || getenv("SSTAT_WIDEP_CLUSTER") || getenv("SSTAT_WIDEP_RING") || getenv("SSTAT_WIDEP_SROWS") || getenv("SSTAT_WIDEP_PERSM") || getenv("SSTAT_WIDEP_R") ||
-                       getenv("SSTAT_WIDEP_WG");
+    // any experiment override: the plan is built for this call only (not cached)
+    bool tuned = false;
+    for (const char* knob : {"SSTAT_WIDEP_CONSUMERS", "SSTAT_WIDEP_NOCLUSTER", "SSTAT_WIDEP_MAXCLUSTER",
+                             "SSTAT_WIDEP_CLUSTER", "SSTAT_WIDEP_RING", "SSTAT_WIDEP_SROWS", "SSTAT_WIDEP_PERSM",
+                             "SSTAT_WIDEP_R", "SSTAT_WIDEP_WG"})
+        tuned = tuned || getenv(knob) != nullptr;
     Plan pl;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
