@@ -512,10 +512,11 @@ def test_buffer_growth_sequence():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("p", [16, 32, 256])
+@pytest.mark.parametrize("p", [9, 16, 32, 256])
 def test_misaligned_device_rows(engine, p):
     """A device pointer that is only 8-byte aligned (a view one double into a buffer) takes
-    the scalar-load / 8-byte cp.async paths and gives the same bits as an aligned copy."""
+    the scalar-load / 8-byte cp.async paths and gives the same bits as an aligned copy (in
+    reference-order mode too: cp.async staging vs the TMA ring)."""
     torch = torch_mod()
     n = 50_001
     buf = torch.empty(n * p + 1, dtype=torch.float64, device="cuda")
@@ -526,6 +527,9 @@ def test_misaligned_device_rows(engine, p):
     assert A.data_ptr() % 16 == 0
     assert engine.dataset_suffstats(D, schema(p), plan(n, 9999)).bit_equal(
         engine.dataset_suffstats(A, schema(p), plan(n, 9999)))
+    if p <= 64:  # reference order: the cp.async-staged kernel (misaligned) vs the TMA ring (aligned)
+        assert engine.dataset_suffstats(D, schema(p), plan(n, 9998), flags=2).bit_equal(
+            engine.dataset_suffstats(A, schema(p), plan(n, 9998), flags=2))
 
 
 def test_widest_fast_path_and_limit(engine, oracle):

@@ -1,1 +1,1 @@
-timeout 900 python bench.py > gpurun_out/bench_default_200.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "misaligned" > gpurun_out/mis_pytest.log 2>&1
