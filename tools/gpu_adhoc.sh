@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "misaligned" > gpurun_out/mis_pytest.log 2>&1
+timeout 600 python tools/register_probe.py 8 > gpurun_out/register_probe.log 2>&1
