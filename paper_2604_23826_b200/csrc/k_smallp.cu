@@ -25,14 +25,16 @@
 namespace sstat_b200 {
 namespace {
 
-template <int NB, bool VEC>
+// X1: p = 8 NB + 1 — the last column rides outside the DMMA blocks (see step()).
+template <int NB, bool VEC, bool X1 = false>
 struct SmallP {
     static constexpr int NBLK = NB * (NB + 1) / 2;
 #ifndef SSTAT_U2V
 #define SSTAT_U2V 16
 #endif
     static constexpr int U = NB <= 2 ? (VEC || NB == 1 ? SSTAT_U2V : 8) : (NB <= 4 ? 8 : 4);  // k-steps in flight per warp
-    static constexpr int FRAG = NBLK * 64 + NB * 8;                // per-warp epilogue values
+    static constexpr int XV = X1 ? NB * 8 + 2 : 0;                 // extra column: x_e x_j, x_e^2, sum
+    static constexpr int FRAG = NBLK * 64 + NB * 8 + XV;           // per-warp epilogue values
     __device__ __forceinline__ static int col(int J, int g) { return VEC ? g * NB + J : J * 8 + g; }
 };
 
@@ -72,11 +74,45 @@ __device__ __forceinline__ void step(const double (&x)[NB], const double (&c)[NB
         for (int K = J; K < NB; ++K, ++b) dmma_8x8x4(acc[b][0], acc[b][1], d[J], d[K]);
 }
 
+// p = 8 NB + 1: a whole DMMA block for one column would spend NB + 1 DMMAs (16 pipe cycles
+// each) on NB * 8 + 1 products per row; instead every lane (g, k) also loads the last column
+// e of its row k (8 lanes, one address) and accumulates d_e * d_{col(J, g)} for each J and
+// d_e^2 with DFMA (2 pipe cycles each), d_e into its sum.  Fixed order per lane, reduced over
+// k and the warps in fixed order in the epilogue: a fixed function of the tile.
+template <int NB>
+__device__ __forceinline__ void step_x1(const double (&x)[NB], double xe, const double (&c)[NB], double ce,
+                                        double (&acc)[NB * (NB + 1) / 2][2], double (&s)[NB], double (&ae)[NB],
+                                        double& aee, double& se) {
+    double d[NB];
+#pragma unroll
+    for (int J = 0; J < NB; ++J) {
+        d[J] = x[J] - c[J];
+        s[J] += d[J];
+    }
+    const double de = xe - ce;
+    se += de;
+    aee = fma(de, de, aee);
+#pragma unroll
+    for (int J = 0; J < NB; ++J) ae[J] = fma(d[J], de, ae[J]);
+    int b = 0;
+#pragma unroll
+    for (int J = 0; J < NB; ++J)
+#pragma unroll
+        for (int K = J; K < NB; ++K, ++b) dmma_8x8x4(acc[b][0], acc[b][1], d[J], d[K]);
+}
+
 // Canonical destination of epilogue value e, or -1 when it is padding or the lower
 // mirror of a diagonal block.
-template <int NB, bool VEC>
+template <int NB, bool VEC, bool X1 = false>
 __device__ int canonical_slot(int e, uint32_t p) {
-    using C = SmallP<NB, VEC>;
+    using C = SmallP<NB, VEC, X1>;
+    if (X1 && e >= C::NBLK * 64 + NB * 8) {  // the extra column 8 NB
+        const int x = e - C::NBLK * 64 - NB * 8;
+        const int ecol = 8 * NB;
+        if (x < NB * 8) return (int)(p + packed_index(p, x, ecol));  // column x = 8 J + g
+        if (x == NB * 8) return (int)(p + packed_index(p, ecol, ecol));
+        return ecol;  // its sum
+    }
     if (e < C::NBLK * 64) {
         int b = e >> 6;
         const int l = (e & 63) >> 1, m = l >> 2, n = 2 * (l & 3) + (e & 1);
@@ -97,9 +133,9 @@ __device__ int canonical_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-template <int NB, bool VEC>
+template <int NB, bool VEC, bool X1 = false>
 __device__ __forceinline__ void smallp_body(const TileJob& job) {
-    using C = SmallP<NB, VEC>;
+    using C = SmallP<NB, VEC, X1>;
     constexpr int U = C::U;
     extern __shared__ double red[];  // [kWarps][FRAG]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -130,34 +166,48 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
         for (int b = 0; b < C::NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
 #pragma unroll
         for (int J = 0; J < NB; ++J) s[J] = 0.0;
+        // X1: the extra column 8 NB (its shift, d_e x d_j per J, d_e^2, sum)
+        const double ce = (X1 && crow != nullptr) ? crow[8 * NB] : 0.0;
+        double ae[NB], aee = 0.0, se = 0.0;
+#pragma unroll
+        for (int J = 0; J < NB; ++J) ae[J] = 0.0;
 
         const uint32_t nks = rows >> 2;
         const uint32_t kstride = kWarps * 4 * p;  // doubles between a warp's consecutive k-steps
         uint32_t ks = warp;
         const double* rowp = tile + (warp * 4 + kk) * p;
         for (; ks + kWarps * (U - 1) < nks; ks += kWarps * U, rowp += U * kstride) {
-            double x[U][NB];
+            double x[U][NB], xe[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) load_row<NB, VEC>(rowp + u * kstride, g, p, x[u]);
+            for (int u = 0; u < U; ++u) {
+                load_row<NB, VEC>(rowp + u * kstride, g, p, x[u]);
+                if (X1) xe[u] = ld_stream(rowp + u * kstride + 8 * NB);
+            }
 #pragma unroll
-            for (int u = 0; u < U; ++u) step<NB>(x[u], c, acc, s);
+            for (int u = 0; u < U; ++u) {
+                if (X1) step_x1<NB>(x[u], xe[u], c, ce, acc, s, ae, aee, se);
+                else step<NB>(x[u], c, acc, s);
+            }
         }
         for (; ks < nks; ks += kWarps, rowp += kstride) {
             double x[NB];
             load_row<NB, VEC>(rowp, g, p, x);
-            step<NB>(x, c, acc, s);
+            if (X1) step_x1<NB>(x, ld_stream(rowp + 8 * NB), c, ce, acc, s, ae, aee, se);
+            else step<NB>(x, c, acc, s);
         }
         // Ragged tail (rows % 4): the warp whose turn k-step nks is; missing rows add 0.
         if ((rows & 3) && warp == (int)(nks % kWarps)) {
             const uint32_t row = nks * 4 + kk;
-            double x[NB];
+            double x[NB], xe = ce;
             if (row < rows) {
                 load_row<NB, VEC>(tile + (uint64_t)row * p, g, p, x);
+                if (X1) xe = ld_stream(tile + (uint64_t)row * p + 8 * NB);
             } else {
 #pragma unroll
                 for (int J = 0; J < NB; ++J) x[J] = c[J];
             }
-            step<NB>(x, c, acc, s);
+            if (X1) step_x1<NB>(x, xe, c, ce, acc, s, ae, aee, se);
+            else step<NB>(x, c, acc, s);
         }
 
         // ---- epilogue: fixed-order reduction to the canonical tile partial ----
@@ -176,13 +226,33 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
 #pragma unroll
             for (int J = 0; J < NB; ++J) mine[C::NBLK * 64 + J * 8 + g] = s[J];
         }
+        if (X1) {  // the extra column, reduced over the 4 rows of a k-step like the sums
+#pragma unroll
+            for (int J = 0; J < NB; ++J) {
+                ae[J] += __shfl_xor_sync(0xffffffffu, ae[J], 1);
+                ae[J] += __shfl_xor_sync(0xffffffffu, ae[J], 2);
+            }
+            aee += __shfl_xor_sync(0xffffffffu, aee, 1);
+            aee += __shfl_xor_sync(0xffffffffu, aee, 2);
+            se += __shfl_xor_sync(0xffffffffu, se, 1);
+            se += __shfl_xor_sync(0xffffffffu, se, 2);
+            double* xm = mine + C::NBLK * 64 + NB * 8;
+            if (kk == 0) {
+#pragma unroll
+                for (int J = 0; J < NB; ++J) xm[J * 8 + g] = ae[J];
+            }
+            if (lane == 0) {
+                xm[NB * 8] = aee;
+                xm[NB * 8 + 1] = se;
+            }
+        }
         __syncthreads();
         double* out = job.tile_partials + t * E;
         for (int e = threadIdx.x; e < C::FRAG; e += kThreads) {
             double v = red[e];
 #pragma unroll
             for (int w = 1; w < kWarps; ++w) v += red[w * C::FRAG + e];
-            const int slot = canonical_slot<NB, VEC>(e, p);
+            const int slot = canonical_slot<NB, VEC, X1>(e, p);
             if (slot >= 0) out[slot] = v;
         }
         __syncthreads();
@@ -203,6 +273,33 @@ __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
 template <int NB, bool VEC, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_smallp_floor(TileJob job) {
     smallp_body<NB, VEC>(job);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads) k_smallp_x1(TileJob job) {
+    smallp_body<NB, false, true>(job);
+}
+
+template <int NB>
+cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
+    constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, false, true>::FRAG;
+    static std::atomic<int> cached[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = dev < 64 ? cached[dev].load() : 0;
+    if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k_smallp_x1<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp_x1<NB>, kThreads, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) per_sm = 1;
+        if (dev < 64) cached[dev].store(per_sm);
+    }
+    const uint64_t tiles = job.tile_end - job.tile_begin;
+    const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
+    if (grid == 0) return cudaSuccess;
+    k_smallp_x1<NB><<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    return cudaGetLastError();
 }
 
 template <int NB, bool VEC>
@@ -249,6 +346,9 @@ cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
     const int nb = (int)((p + 7) / 8);
     // 128-bit loads need p a multiple of 16 and a 16-byte aligned base.
     const bool vec = (p == 8u * nb) && (nb % 2 == 0) && (reinterpret_cast<uintptr_t>(job.base) % 16 == 0);
+    // p = 9 / 17: the last column by DFMA instead of a nearly empty block row of DMMAs
+    if (p == 9 && !getenv("SSTAT_K1_NO_X1")) return launch_nb_x1<1>(job, sms, stream);
+    if (p == 17 && !getenv("SSTAT_K1_NO_X1")) return launch_nb_x1<2>(job, sms, stream);
     switch (nb) {
         case 1: return launch_nb<1, false>(job, sms, stream);
         case 2: return vec ? launch_nb<2, true>(job, sms, stream) : launch_nb<2, false>(job, sms, stream);

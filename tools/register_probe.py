@@ -7,6 +7,7 @@ import os
 import sys
 import time
 
+import numpy as np
 import torch
 
 gb = float(sys.argv[1]) if len(sys.argv) > 1 else 4.0
@@ -26,7 +27,7 @@ if cudart is None:
     cudart = ctypes.CDLL(cands[0])
 fd = os.open(path, os.O_RDWR)
 mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
-import numpy as np
+
 arr = np.frombuffer(mm, dtype=np.uint8)
 addr = arr.ctypes.data
 dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
