@@ -346,9 +346,22 @@ cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
     const int nb = (int)((p + 7) / 8);
     // 128-bit loads need p a multiple of 16 and a 16-byte aligned base.
     const bool vec = (p == 8u * nb) && (nb % 2 == 0) && (reinterpret_cast<uintptr_t>(job.base) % 16 == 0);
-    // p = 9 / 17: the last column by DFMA instead of a nearly empty block row of DMMAs
-    if (p == 9 && !getenv("SSTAT_K1_NO_X1")) return launch_nb_x1<1>(job, sms, stream);
-    if (p == 17 && !getenv("SSTAT_K1_NO_X1")) return launch_nb_x1<2>(job, sms, stream);
+    // p = 8 NB + 1: the last column by DFMA instead of a nearly empty block row of DMMAs
+    // (measured, profiles/r01_k1_x1.log: p = 9 / 17 / 25 / 41 / 49 / 57 +43 / +4 / +20 / +42 /
+    // +4 / +8 %)
+    if (p % 8 == 1 && p > 1 && !getenv("SSTAT_K1_NO_X1")) {
+        switch (p / 8) {
+            case 1: return launch_nb_x1<1>(job, sms, stream);
+            case 2: return launch_nb_x1<2>(job, sms, stream);
+            case 3: return launch_nb_x1<3>(job, sms, stream);
+            // NB = 4 (p = 33): 136 registers, one CTA per SM — measured 18 % below the
+            // occupancy-floored 5-block-row kernel, which it keeps
+            case 5: return launch_nb_x1<5>(job, sms, stream);
+            case 6: return launch_nb_x1<6>(job, sms, stream);
+            case 7: return launch_nb_x1<7>(job, sms, stream);
+            default: break;
+        }
+    }
     switch (nb) {
         case 1: return launch_nb<1, false>(job, sms, stream);
         case 2: return vec ? launch_nb<2, true>(job, sms, stream) : launch_nb<2, false>(job, sms, stream);
