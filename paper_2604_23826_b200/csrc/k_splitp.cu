@@ -23,10 +23,13 @@ namespace {
 
 constexpr int kU = 2;  // k-steps of loads in flight per warp
 
-template <int NB>
+// X1: p = 8 NB + 1 — the last column rides outside the DMMA blocks, as in K1's
+// k_smallp_x1: part 0 accumulates d_e d_j (j < 8 NB), d_e^2 and the sum of d_e with DFMA.
+template <int NB, bool X1 = false>
 struct SplitP {
     static constexpr int NBLK = NB * (NB + 1) / 2;
-    static constexpr int FRAG = NBLK * 64 + NB * 8;  // per-group epilogue values
+    static constexpr int XV = X1 ? NB * 8 + 2 : 0;     // extra column: x_e x_j, x_e^2, sum
+    static constexpr int FRAG = NBLK * 64 + NB * 8 + XV;  // per-group epilogue values
 };
 
 template <int NB, int W, int PART>
@@ -43,14 +46,27 @@ __device__ __forceinline__ void load_k(const double* __restrict__ rowp, int g, u
     }
 }
 
-template <int NB, int W, int PART>
-__device__ __forceinline__ void split_step(const double (&x)[NB], const double (&c)[NB],
-                                           double (&acc)[Mine<NB, W, PART>::N][2], double (&s)[NB]) {
+// The extra column's state (X1, part 0 only): shift, products with each J, square, sum.
+template <int NB>
+struct Extra {
+    double ce, ae[NB], aee, se;
+};
+
+template <int NB, int W, int PART, bool X1>
+__device__ __forceinline__ void split_step(const double (&x)[NB], double xe, const double (&c)[NB],
+                                           double (&acc)[Mine<NB, W, PART>::N][2], double (&s)[NB], Extra<NB>& ex) {
     double d[NB];
 #pragma unroll
     for (int J = 0; J < NB; ++J) {
         d[J] = x[J] - c[J];
         if (PART == 0) s[J] += d[J];
+    }
+    if (X1 && PART == 0) {
+        const double de = xe - ex.ce;
+        ex.se += de;
+        ex.aee = fma(de, de, ex.aee);
+#pragma unroll
+        for (int J = 0; J < NB; ++J) ex.ae[J] = fma(d[J], de, ex.ae[J]);
     }
     int b = 0;
 #pragma unroll
@@ -62,9 +78,15 @@ __device__ __forceinline__ void split_step(const double (&x)[NB], const double (
 
 // Canonical destination of epilogue value e (block values, then the sums) or -1
 // (padding / lower mirror of a diagonal block); columns col(J, g) = 8 J + g.
-template <int NB>
+template <int NB, bool X1>
 __device__ int split_slot(int e, uint32_t p) {
     constexpr int NBLK = SplitP<NB>::NBLK;
+    if (X1 && e >= NBLK * 64 + NB * 8) {  // the extra column 8 NB
+        const int x = e - NBLK * 64 - NB * 8, ecol = 8 * NB;
+        if (x < NB * 8) return (int)(p + packed_index(p, x, ecol));  // column x = 8 J + g
+        if (x == NB * 8) return (int)(p + packed_index(p, ecol, ecol));
+        return ecol;  // its sum
+    }
     if (e < NBLK * 64) {
         int b = e >> 6;
         const int l = (e & 63) >> 1, m = l >> 2, n = 2 * (l & 3) + (e & 1);
@@ -84,9 +106,10 @@ __device__ int split_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-template <int NB, int W, int PART>
+template <int NB, int W, int PART, bool X1>
 __device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_rows, double* red) {
-    using C = SplitP<NB>;
+    using C = SplitP<NB, X1>;
+    constexpr bool XP = X1 && PART == 0;  // this warp carries the extra column
     constexpr int G = kWarps / W;  // row groups
     constexpr int NM = Mine<NB, W, PART>::N;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,34 +134,43 @@ __device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_row
         for (int b = 0; b < NM; ++b) acc[b][0] = acc[b][1] = 0.0;
 #pragma unroll
         for (int J = 0; J < NB; ++J) s[J] = 0.0;
+        Extra<NB> ex;
+        ex.ce = (XP && crow != nullptr) ? crow[8 * NB] : 0.0;
+        ex.aee = ex.se = 0.0;
+#pragma unroll
+        for (int J = 0; J < NB; ++J) ex.ae[J] = 0.0;
 
         const uint32_t nks = rows >> 2;
         const uint64_t kstride = (uint64_t)G * 4 * p;
         uint32_t ks = group;
         const double* rowp = tile + (uint64_t)(group * 4 + kk) * p;
         for (; ks + G * (kU - 1) < nks; ks += G * kU, rowp += kU * kstride) {
-            double x[kU][NB];
+            double x[kU][NB], xe[kU];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) load_k<NB>(rowp + u * kstride, g, p, x[u]);
+            for (int u = 0; u < kU; ++u) {
+                load_k<NB>(rowp + u * kstride, g, p, x[u]);
+                xe[u] = XP ? __ldg(rowp + u * kstride + 8 * NB) : 0.0;
+            }
 #pragma unroll
-            for (int u = 0; u < kU; ++u) split_step<NB, W, PART>(x[u], c, acc, s);
+            for (int u = 0; u < kU; ++u) split_step<NB, W, PART, X1>(x[u], xe[u], c, acc, s, ex);
         }
         for (; ks < nks; ks += G, rowp += kstride) {
             double x[NB];
             load_k<NB>(rowp, g, p, x);
-            split_step<NB, W, PART>(x, c, acc, s);
+            split_step<NB, W, PART, X1>(x, XP ? __ldg(rowp + 8 * NB) : 0.0, c, acc, s, ex);
         }
         // ragged tail (rows % 4): the group whose turn k-step nks is; missing rows add 0
         if ((rows & 3) && group == (int)(nks % G)) {
             const uint32_t row = nks * 4 + kk;
-            double x[NB];
+            double x[NB], xe = ex.ce;
             if (row < rows) {
                 load_k<NB>(tile + (uint64_t)row * p, g, p, x);
+                if (XP) xe = __ldg(tile + (uint64_t)row * p + 8 * NB);
             } else {
 #pragma unroll
                 for (int J = 0; J < NB; ++J) x[J] = c[J];
             }
-            split_step<NB, W, PART>(x, c, acc, s);
+            split_step<NB, W, PART, X1>(x, xe, c, acc, s, ex);
         }
 
         // ---- epilogue: each group's partial into red[group], then the groups in order ----
@@ -165,10 +197,30 @@ __device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_row
                 for (int J = 0; J < NB; ++J) mine[C::NBLK * 64 + J * 8 + g] = s[J];
             }
         }
+        if (XP) {  // the extra column, reduced over the 4 rows of a k-step like the sums
+#pragma unroll
+            for (int J = 0; J < NB; ++J) {
+                ex.ae[J] += __shfl_xor_sync(0xffffffffu, ex.ae[J], 1);
+                ex.ae[J] += __shfl_xor_sync(0xffffffffu, ex.ae[J], 2);
+            }
+            ex.aee += __shfl_xor_sync(0xffffffffu, ex.aee, 1);
+            ex.aee += __shfl_xor_sync(0xffffffffu, ex.aee, 2);
+            ex.se += __shfl_xor_sync(0xffffffffu, ex.se, 1);
+            ex.se += __shfl_xor_sync(0xffffffffu, ex.se, 2);
+            double* xm = mine + C::NBLK * 64 + NB * 8;
+            if (kk == 0) {
+#pragma unroll
+                for (int J = 0; J < NB; ++J) xm[J * 8 + g] = ex.ae[J];
+            }
+            if (lane == 0) {
+                xm[NB * 8] = ex.aee;
+                xm[NB * 8 + 1] = ex.se;
+            }
+        }
         __syncthreads();
         double* out = job.tile_partials + t * E;
         for (int e = threadIdx.x; e < C::FRAG; e += kThreads) {
-            const int slot = split_slot<NB>(e, p);
+            const int slot = split_slot<NB, X1>(e, p);
             if (slot < 0) continue;
             double v = red[e];
 #pragma unroll
@@ -179,38 +231,38 @@ __device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_row
     }
 }
 
-template <int NB, int W>
+template <int NB, int W, bool X1>
 __global__ void __launch_bounds__(kThreads, 1) k_splitp(TileJob job, uint32_t tile_rows) {
     extern __shared__ double red[];  // [8 / W][FRAG]
     const int part = (threadIdx.x >> 5) % W;
-    if (part == 0) split_body<NB, W, 0>(job, tile_rows, red);
-    else if (part == 1) split_body<NB, W, 1>(job, tile_rows, red);
+    if (part == 0) split_body<NB, W, 0, X1>(job, tile_rows, red);
+    else if (part == 1) split_body<NB, W, 1, X1>(job, tile_rows, red);
     else if constexpr (W == 4) {
-        if (part == 2) split_body<NB, W, 2>(job, tile_rows, red);
-        else split_body<NB, W, 3>(job, tile_rows, red);
+        if (part == 2) split_body<NB, W, 2, X1>(job, tile_rows, red);
+        else split_body<NB, W, 3, X1>(job, tile_rows, red);
     }
 }
 
-template <int NB, int W>
+template <int NB, int W, bool X1 = false>
 cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
-    constexpr size_t smem = sizeof(double) * (kWarps / W) * SplitP<NB>::FRAG;
+    constexpr size_t smem = sizeof(double) * (kWarps / W) * SplitP<NB, X1>::FRAG;
     static std::atomic<int> cached[64];
     int dev = 0;
     cudaGetDevice(&dev);
     int per_sm = dev < 64 ? cached[dev].load() : 0;
     if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_splitp<NB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_splitp<NB, W, X1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_splitp<NB, W>, kThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_splitp<NB, W, X1>, kThreads, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
-        if (getenv("SSTAT_DEBUG")) fprintf(stderr, "k_splitp<%d,%d>: smem=%zu per_sm=%d\n", NB, W, smem, per_sm);
+        if (getenv("SSTAT_DEBUG")) fprintf(stderr, "k_splitp<%d,%d,%d>: smem=%zu per_sm=%d\n", NB, W, (int)X1, smem, per_sm);
         if (dev < 64) cached[dev].store(per_sm);
     }
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
-    k_splitp<NB, W><<<(unsigned)grid, kThreads, smem, stream>>>(job, widep_tile_rows(job.p));
+    k_splitp<NB, W, X1><<<(unsigned)grid, kThreads, smem, stream>>>(job, widep_tile_rows(job.p));
     return cudaGetLastError();
 }
 
@@ -224,10 +276,27 @@ bool splitp_handles(uint32_t p) {
         if (atoi(env) == 0) return false;
     }
     const uint32_t nb = (p + 7) / 8;
-    return p > 64 && p <= 128 && nb != 12;
+    const bool x1 = p == 89 && !getenv("SSTAT_K1W_NO_X1");  // 11 block rows + the extra column
+    return p > 64 && p <= 128 && (nb != 12 || x1);
 }
 
 cudaError_t launch_splitp(const TileJob& job, int sms, cudaStream_t stream) {
+    // p = 8 NB + 1: NB block rows plus the last column by DFMA (k_smallp_x1's scheme) instead
+    // of NB + 1 block rows whose last one holds a single column (measured,
+    // profiles/r01_k1w_x1.log: p = 65 / 73 / 81 / 105 / 113 +7 / +9 / +11 / +7 / +1 %, p = 89
+    // +23 % over K2).  p = 97 (NB = 12) keeps the 13-block-row W = 4 split (the 12-block splits
+    // are slow, above); p = 121 keeps NB = 16 (the NB = 15 x1 instance spills: -19 %).
+    if (job.p % 8 == 1 && !getenv("SSTAT_K1W_NO_X1")) {
+        switch (job.p / 8) {
+            case 8: return launch_nb<8, 2, true>(job, sms, stream);
+            case 9: return launch_nb<9, 2, true>(job, sms, stream);
+            case 10: return launch_nb<10, 2, true>(job, sms, stream);
+            case 11: return launch_nb<11, 2, true>(job, sms, stream);
+            case 13: return launch_nb<13, 4, true>(job, sms, stream);
+            case 14: return launch_nb<14, 4, true>(job, sms, stream);
+            default: break;
+        }
+    }
     switch ((job.p + 7) / 8) {
         case 9: return launch_nb<9, 2>(job, sms, stream);
         case 10: return launch_nb<10, 2>(job, sms, stream);

@@ -471,6 +471,28 @@ def test_wide_p_shapes_vs_truth(engine, oracle, p):
     assert np.array_equal(bits(got.cross[[0, 1, p]]), bits(tS[[0, 1, p]]))  # integer block exact
 
 
+@pytest.mark.parametrize("p", [65, 73, 81, 89, 97, 105, 113, 121])
+def test_k1w_extra_column_widths(engine, p, monkeypatch):
+    """p = 8 NB + 1 in K1w: NB block rows plus the last column by DFMA (part 0 of each row
+    group) against the 80-bit truth, integer block bit-exact, ragged tiles and ranges; the
+    (NB + 1)-block-row split (SSTAT_K1W_NO_X1) agrees within the same tolerance."""
+    rng = np.random.default_rng(1000 + p)
+    n = 70001
+    X = rng.normal(-0.5, 1.5, size=(n, p))
+    X[:, 0] = rng.integers(1, 100, size=n)
+    X[:, p - 1] = rng.integers(1, 100, size=n)  # the extra column itself integer-valued
+    ts, tS = truth_suffstats(X)
+    D = to_dev(X)
+    got = engine.dataset_suffstats(D, schema(p), plan(n, 33331))
+    check_against(got, n, ts, tS)
+    last = p - 1
+    exact = [0, last, last * p - last * (last - 1) // 2]  # Σx0², Σx0·x_last, Σx_last² (SymPacked)
+    assert np.array_equal(bits(got.cross[exact]), bits(tS[exact]))
+    assert np.array_equal(bits(got.sums[[0, last]]), bits(ts[[0, last]]))
+    monkeypatch.setenv("SSTAT_K1W_NO_X1", "1")
+    check_against(engine.dataset_suffstats(D, schema(p), plan(n, 33331)), n, ts, tS)
+
+
 def test_every_p_up_to_72(engine):
     """Every width through K1's template instances (column blocks 1..8, vector and scalar
     loads) and across the K1 -> K2 switch at p = 64 / 65, ragged tiles and ranges: the
