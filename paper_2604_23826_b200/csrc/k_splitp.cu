@@ -21,7 +21,7 @@
 namespace sstat_b200 {
 namespace {
 
-constexpr int kU = 2;  // k-steps of loads in flight per warp
+constexpr int kU = 2;  // k-steps of loads in flight per warp (default; U below)
 
 // X1: p = 8 NB + 1 — the last column rides outside the DMMA blocks, as in K1's
 // k_smallp_x1: part 0 accumulates d_e d_j (j < 8 NB), d_e^2 and the sum of d_e with DFMA.
@@ -106,7 +106,7 @@ __device__ int split_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-template <int NB, int W, int PART, bool X1>
+template <int NB, int W, int PART, bool X1, int kU>
 __device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_rows, double* red) {
     using C = SplitP<NB, X1>;
     constexpr bool XP = X1 && PART == 0;  // this warp carries the extra column
@@ -231,19 +231,19 @@ __device__ __forceinline__ void split_body(const TileJob& job, uint32_t tile_row
     }
 }
 
-template <int NB, int W, bool X1>
+template <int NB, int W, bool X1, int U>
 __global__ void __launch_bounds__(kThreads, 1) k_splitp(TileJob job, uint32_t tile_rows) {
     extern __shared__ double red[];  // [8 / W][FRAG]
     const int part = (threadIdx.x >> 5) % W;
-    if (part == 0) split_body<NB, W, 0, X1>(job, tile_rows, red);
-    else if (part == 1) split_body<NB, W, 1, X1>(job, tile_rows, red);
+    if (part == 0) split_body<NB, W, 0, X1, U>(job, tile_rows, red);
+    else if (part == 1) split_body<NB, W, 1, X1, U>(job, tile_rows, red);
     else if constexpr (W == 4) {
-        if (part == 2) split_body<NB, W, 2, X1>(job, tile_rows, red);
-        else split_body<NB, W, 3, X1>(job, tile_rows, red);
+        if (part == 2) split_body<NB, W, 2, X1, U>(job, tile_rows, red);
+        else split_body<NB, W, 3, X1, U>(job, tile_rows, red);
     }
 }
 
-template <int NB, int W, bool X1 = false>
+template <int NB, int W, bool X1 = false, int U = kU>
 cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * (kWarps / W) * SplitP<NB, X1>::FRAG;
     static std::atomic<int> cached[64];
@@ -251,9 +251,9 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     cudaGetDevice(&dev);
     int per_sm = dev < 64 ? cached[dev].load() : 0;
     if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_splitp<NB, W, X1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_splitp<NB, W, X1, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_splitp<NB, W, X1>, kThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_splitp<NB, W, X1, U>, kThreads, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
         if (getenv("SSTAT_DEBUG")) fprintf(stderr, "k_splitp<%d,%d,%d>: smem=%zu per_sm=%d\n", NB, W, (int)X1, smem, per_sm);
@@ -262,8 +262,29 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
-    k_splitp<NB, W, X1><<<(unsigned)grid, kThreads, smem, stream>>>(job, widep_tile_rows(job.p));
+    k_splitp<NB, W, X1, U><<<(unsigned)grid, kThreads, smem, stream>>>(job, widep_tile_rows(job.p));
     return cudaGetLastError();
+}
+
+// k-steps of loads in flight per warp, per instance (SSTAT_K1W_U overrides: 2, 3 or 4).
+// K1w runs one CTA (8 warps) per SM, so its loads are latency-bound where the registers allow
+// more in flight.  Measured (profiles/r01_k1w_u.log, TF/s at U = 2 -> chosen): p = 65 15.3 ->
+// 19.2 (U = 4), p = 72 21.7 -> 25.6, p = 73 21.9 -> 24.2, p = 80 21.4 -> 24.2, p = 104 21.7 ->
+// 25.0, p = 105 21.9 -> 22.4, p = 112 21.0 -> 21.3 (U = 3); the others lose with U > 2.
+template <int NB, bool X1>
+constexpr int default_u() {
+    if (NB == 8 && X1) return 4;
+    if (NB == 9 || (NB == 10 && !X1) || NB == 13 || (NB == 14 && !X1)) return 3;
+    return 2;
+}
+
+template <int NB, int W, bool X1>
+cudaError_t launch_u(const TileJob& job, int sms, cudaStream_t stream) {
+    int u = default_u<NB, X1>();
+    if (const char* env = getenv("SSTAT_K1W_U")) u = atoi(env);
+    if (u == 3) return launch_nb<NB, W, X1, 3>(job, sms, stream);
+    if (u == 4) return launch_nb<NB, W, X1, 4>(job, sms, stream);
+    return launch_nb<NB, W, X1, 2>(job, sms, stream);
 }
 
 }  // namespace
@@ -288,23 +309,23 @@ cudaError_t launch_splitp(const TileJob& job, int sms, cudaStream_t stream) {
     // are slow, above); p = 121 keeps NB = 16 (the NB = 15 x1 instance spills: -19 %).
     if (job.p % 8 == 1 && !getenv("SSTAT_K1W_NO_X1")) {
         switch (job.p / 8) {
-            case 8: return launch_nb<8, 2, true>(job, sms, stream);
-            case 9: return launch_nb<9, 2, true>(job, sms, stream);
-            case 10: return launch_nb<10, 2, true>(job, sms, stream);
-            case 11: return launch_nb<11, 2, true>(job, sms, stream);
-            case 13: return launch_nb<13, 4, true>(job, sms, stream);
-            case 14: return launch_nb<14, 4, true>(job, sms, stream);
+            case 8: return launch_u<8, 2, true>(job, sms, stream);
+            case 9: return launch_u<9, 2, true>(job, sms, stream);
+            case 10: return launch_u<10, 2, true>(job, sms, stream);
+            case 11: return launch_u<11, 2, true>(job, sms, stream);
+            case 13: return launch_u<13, 4, true>(job, sms, stream);
+            case 14: return launch_u<14, 4, true>(job, sms, stream);
             default: break;
         }
     }
     switch ((job.p + 7) / 8) {
-        case 9: return launch_nb<9, 2>(job, sms, stream);
-        case 10: return launch_nb<10, 2>(job, sms, stream);
-        case 11: return launch_nb<11, 2>(job, sms, stream);
-        case 13: return launch_nb<13, 4>(job, sms, stream);
-        case 14: return launch_nb<14, 4>(job, sms, stream);
-        case 15: return launch_nb<15, 4>(job, sms, stream);
-        case 16: return launch_nb<16, 4>(job, sms, stream);
+        case 9: return launch_u<9, 2, false>(job, sms, stream);
+        case 10: return launch_u<10, 2, false>(job, sms, stream);
+        case 11: return launch_u<11, 2, false>(job, sms, stream);
+        case 13: return launch_u<13, 4, false>(job, sms, stream);
+        case 14: return launch_u<14, 4, false>(job, sms, stream);
+        case 15: return launch_u<15, 4, false>(job, sms, stream);
+        case 16: return launch_u<16, 4, false>(job, sms, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -493,6 +493,22 @@ def test_k1w_extra_column_widths(engine, p, monkeypatch):
     check_against(engine.dataset_suffstats(D, schema(p), plan(n, 33331)), n, ts, tS)
 
 
+@pytest.mark.parametrize("p", [65, 72, 81, 97, 104, 128])
+def test_k1w_load_depth_bit_identical(engine, p, monkeypatch):
+    """K1w's loads in flight (U = 2 / 3 / 4 k-steps, SSTAT_K1W_U) only batch the loads: each
+    warp accumulates the same k-steps in the same order, so every depth gives the same bits."""
+    torch = torch_mod()
+    n = 90001
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 2, 5, 1.0, 0, 0, n, p)
+    pl = plan(n, 40009)
+    base = engine.dataset_suffstats(D, schema(p), pl)
+    for u in ("2", "3", "4"):
+        with monkeypatch.context() as m:
+            m.setenv("SSTAT_K1W_U", u)
+            assert engine.dataset_suffstats(D, schema(p), pl).bit_equal(base), u
+
+
 def test_every_p_up_to_72(engine):
     """Every width through K1's template instances (column blocks 1..8, vector and scalar
     loads) and across the K1 -> K2 switch at p = 64 / 65, ragged tiles and ranges: the
