@@ -271,9 +271,11 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
 // more in flight.  Measured (profiles/r01_k1w_u.log, TF/s at U = 2 -> chosen): p = 65 15.3 ->
 // 19.2 (U = 4), p = 72 21.7 -> 25.6, p = 73 21.9 -> 24.2, p = 80 21.4 -> 24.2, p = 104 21.7 ->
 // 25.0, p = 105 21.9 -> 22.4, p = 112 21.0 -> 21.3 (U = 3); the others lose with U > 2.
+// NB = 12 (p = 90-96) with W = 4 at U = 4: p = 92 / 96 17.7 / 16.5 against K2's 15.1 / 16.0
+// (U = 2: 14.0 / 13.6; W = 2 spills at every U: 10-14) — profiles/r01_k1w_nb12.log.
 template <int NB, bool X1>
 constexpr int default_u() {
-    if (NB == 8 && X1) return 4;
+    if ((NB == 8 && X1) || NB == 12) return 4;
     if (NB == 9 || (NB == 10 && !X1) || NB == 13 || (NB == 14 && !X1)) return 3;
     return 2;
 }
@@ -290,23 +292,22 @@ cudaError_t launch_u(const TileJob& job, int sms, cudaStream_t stream) {
 }  // namespace
 
 // Measured (profiles/r01_p_sweep.log): W = 2 for NB = 9..11 (21-22 TF/s vs K2's 8.5-17.5),
-// W = 4 for NB = 13..16 (20-22 TF/s vs 14-21); at NB = 12 both splits stay near 14 TF/s and
-// K2's 2x2 rectangles do better (16), so p = 89..96 keeps K2.
+// W = 4 for NB = 12..16 (20-22 TF/s vs 14-21; NB = 12 only with 4 k-steps of loads in flight,
+// default_u above), so K1w takes every 64 < p <= 128 (SSTAT_SPLITP=0: K2 there).
 bool splitp_handles(uint32_t p) {
     if (const char* env = getenv("SSTAT_SPLITP")) {
         if (atoi(env) == 0) return false;
     }
-    const uint32_t nb = (p + 7) / 8;
-    const bool x1 = p == 89 && !getenv("SSTAT_K1W_NO_X1");  // 11 block rows + the extra column
-    return p > 64 && p <= 128 && (nb != 12 || x1);
+    return p > 64 && p <= 128;
 }
 
 cudaError_t launch_splitp(const TileJob& job, int sms, cudaStream_t stream) {
     // p = 8 NB + 1: NB block rows plus the last column by DFMA (k_smallp_x1's scheme) instead
     // of NB + 1 block rows whose last one holds a single column (measured,
     // profiles/r01_k1w_x1.log: p = 65 / 73 / 81 / 105 / 113 +7 / +9 / +11 / +7 / +1 %, p = 89
-    // +23 % over K2).  p = 97 (NB = 12) keeps the 13-block-row W = 4 split (the 12-block splits
-    // are slow, above); p = 121 keeps NB = 16 (the NB = 15 x1 instance spills: -19 %).
+    // +23 % over K2); p = 97 keeps the 13-block-row split (the 12-row extra-column instance sits
+    // at 254 registers: 13.9 vs 14.7 TF/s at its best U, profiles/r01_k1w_nb12.log) and p = 121
+    // NB = 16 (the NB = 15 x1 instance spills: -19 %).
     if (job.p % 8 == 1 && !getenv("SSTAT_K1W_NO_X1")) {
         switch (job.p / 8) {
             case 8: return launch_u<8, 2, true>(job, sms, stream);
@@ -322,6 +323,7 @@ cudaError_t launch_splitp(const TileJob& job, int sms, cudaStream_t stream) {
         case 9: return launch_u<9, 2, false>(job, sms, stream);
         case 10: return launch_u<10, 2, false>(job, sms, stream);
         case 11: return launch_u<11, 2, false>(job, sms, stream);
+        case 12: return launch_u<12, 4, false>(job, sms, stream);
         case 13: return launch_u<13, 4, false>(job, sms, stream);
         case 14: return launch_u<14, 4, false>(job, sms, stream);
         case 15: return launch_u<15, 4, false>(job, sms, stream);

@@ -493,7 +493,7 @@ def test_k1w_extra_column_widths(engine, p, monkeypatch):
     check_against(engine.dataset_suffstats(D, schema(p), plan(n, 33331)), n, ts, tS)
 
 
-@pytest.mark.parametrize("p", [65, 72, 81, 97, 104, 128])
+@pytest.mark.parametrize("p", [65, 72, 81, 92, 96, 97, 104, 128])
 def test_k1w_load_depth_bit_identical(engine, p, monkeypatch):
     """K1w's loads in flight (U = 2 / 3 / 4 k-steps, SSTAT_K1W_U) only batch the loads: each
     warp accumulates the same k-steps in the same order, so every depth gives the same bits."""
