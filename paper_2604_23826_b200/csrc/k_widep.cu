@@ -732,11 +732,11 @@ void free_plan(const Plan& pl) {
 
 // The launch geometry for width p with the 4/8-warp kernel (wg = false) or k_widep_wg, plus the
 // cluster-less side plan for the CTA slots its cluster placement leaves idle.
-cudaError_t build_plan(int device, uint32_t p, uint32_t srows, bool wg, Plan& pl) {
+cudaError_t build_plan(int device, uint32_t p, uint32_t srows, bool wg, Plan& pl, uint32_t force_r = 0) {
     WideGeom geo{};
     geo.p = p;
     geo.nb = (p + 7) / 8;
-    geo.R = env_u32("SSTAT_WIDEP_R", choose_r(geo.nb, wg ? kWgConsumers : 4));
+    geo.R = env_u32("SSTAT_WIDEP_R", force_r ? force_r : choose_r(geo.nb, wg ? kWgConsumers : 4));
     if (geo.R < 2 || geo.R > 4) geo.R = 4;
     geo.nr = (geo.nb + geo.R - 1) / geo.R;
     // pitch = 4 (mod 16) doubles puts the 4 rows of a k-step in distinct 32-byte bank
@@ -818,6 +818,12 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
                 e = build_plan(device, p, srows, atoi(wg_env) != 0, pl);
             } else if (nb <= 16) {
                 e = build_plan(device, p, srows, false, pl);
+            } else if (nb <= 25 && nb != 18) {
+                // p = 129-200 except 137-144: the 4-warp kernel with 3x3 rectangles beats the
+                // efficiency model's pick (measured, profiles/r01_k2_r_window.log: p = 130 / 136 /
+                // 152 / 160 / 176 / 184 / 192 / 200 +12 / +11 / +26 / +24 / +26 / +8 / +8 / +8 %;
+                // p = 144 keeps the model's plan, 3x3 there is -11 %)
+                e = build_plan(device, p, srows, false, pl, 3);
             } else {
                 Plan pc, pw;
                 e = build_plan(device, p, srows, false, pc);
