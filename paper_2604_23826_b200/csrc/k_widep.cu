@@ -818,11 +818,12 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
                 e = build_plan(device, p, srows, atoi(wg_env) != 0, pl);
             } else if (nb <= 16) {
                 e = build_plan(device, p, srows, false, pl);
-            } else if (nb <= 25 && nb != 18) {
-                // p = 129-200 except 137-144: the 4-warp kernel with 3x3 rectangles beats the
-                // efficiency model's pick (measured, profiles/r01_k2_r_window.log: p = 130 / 136 /
-                // 152 / 160 / 176 / 184 / 192 / 200 +12 / +11 / +26 / +24 / +26 / +8 / +8 / +8 %;
-                // p = 144 keeps the model's plan, 3x3 there is -11 %)
+            } else if ((nb <= 25 && nb != 18) || nb == 29 || nb == 30) {
+                // p = 129-200 except 137-144, and p = 225-240: the 4-warp kernel with 3x3
+                // rectangles beats the efficiency model's pick (measured,
+                // profiles/r01_k2_r_window.log: p = 130 / 136 / 152 / 160 / 176 / 184 / 192 / 200
+                // +12 / +11 / +26 / +24 / +26 / +8 / +8 / +8 %, p = 232 / 240 +11 / +12 %;
+                // p = 144, 216, 264-320 keep the model's plan)
                 e = build_plan(device, p, srows, false, pl, 3);
             } else {
                 Plan pc, pw;
