@@ -39,6 +39,7 @@
  *   SSTAT_ERR_IO / _FORMAT  IoError / FormatError (file sources)         errors.hpp:18-30
  *   SSTAT_ERR_UNSUPPORTED  also: p > 2048 columns outside reference-order mode (the fast
  *                        path stages whole rows in shared memory)
+ *   SSTAT_ERR_PEER       another rank of the communicator failed
  *   SSTAT_ERR_CUDA / _NCCL / _OOM / _UNSUPPORTED  device-side failures (no reference
  *                        equivalent; the glue throws sstat::Error).
  *
@@ -56,7 +57,7 @@
 extern "C" {
 #endif
 
-#define SSTAT_CUDA_ABI_VERSION 1
+#define SSTAT_CUDA_ABI_VERSION 2
 
 typedef enum {
     SSTAT_OK = 0,
@@ -68,7 +69,8 @@ typedef enum {
     SSTAT_ERR_OOM = 6,
     SSTAT_ERR_UNSUPPORTED = 7,
     SSTAT_ERR_IO = 8,
-    SSTAT_ERR_FORMAT = 9
+    SSTAT_ERR_FORMAT = 9,
+    SSTAT_ERR_PEER = 10 /* another rank of the communicator failed (its status is in msg)  */
 } sstat_status;
 
 /* PrecisionMode (reduce.hpp:40-45). */
@@ -114,16 +116,28 @@ typedef struct {
 typedef enum {
     SSTAT_SRC_DEVICE = 0, /* ptr is device memory on the context's device          */
     SSTAT_SRC_HOST = 1,   /* ptr is host memory (pinned: direct DMA; else staged)  */
-    SSTAT_SRC_FILE = 2    /* path names an SSTATBIN file (binfile.hpp:17-29)        */
+    SSTAT_SRC_FILE = 2,   /* path names an SSTATBIN file (binfile.hpp:17-29)        */
+    SSTAT_SRC_READER = 3  /* rows come from read_rows (below)                       */
 } sstat_source_kind;
+
+/* The reader of an SSTAT_SRC_READER source: BinaryReader::read_rows (reference
+ * src/binfile.cpp:140-161) as a C callback.  The engine asks for rows [first_row, first_row +
+ * n_rows) (whole staging slots, ascending, one call at a time per device) and the callback
+ * either copies them into `scratch` (pinned staging memory of n_rows * p * 8 bytes) and returns
+ * scratch, or returns a pointer to host memory already holding them (pinned memory is copied to
+ * the device by DMA directly) that stays valid until the pass returns.  NULL = the read failed
+ * (SSTAT_ERR_IO).  Lets a dataset larger than host memory stream through the pinned ring. */
+typedef const void* (*sstat_read_rows_fn)(void* user, uint64_t first_row, uint64_t n_rows, void* scratch);
 
 typedef struct {
     uint32_t kind;        /* sstat_source_kind                                       */
     uint32_t reserved;
     const void* ptr;      /* DEVICE/HOST: rows [first_row, first_row + n_rows)       */
-    uint64_t first_row;   /* absolute dataset row held at ptr[0]                     */
-    uint64_t n_rows;      /* rows addressable through ptr                            */
+    uint64_t first_row;   /* absolute dataset row held at ptr[0] (READER: first row  */
+    uint64_t n_rows;      /* rows addressable (READER: rows read_rows can serve)     */
     const char* path;     /* FILE                                                    */
+    sstat_read_rows_fn read_rows; /* READER                                          */
+    void* user;           /* READER: passed to read_rows                             */
 } sstat_cuda_source;
 
 /* ---- library / context ---- */
@@ -132,10 +146,32 @@ const char* sstat_status_string(int status);
 
 /* One context per process per device.  device < 0 selects the current device. */
 int sstat_cuda_init(sstat_cuda_ctx** ctx, int device);
+
+/* A device group: one process driving n_gpus devices (SURVEY.md §8(b) Export 1; the paper's
+ * single host process over all GPUs).  Member i is rank i of n_gpus: the plan's
+ * ranges are sharded contiguously exactly as in the multi-process path (sstat_shard_ranges),
+ * every member accumulates its share in parallel on its own host thread, and the rank buffers
+ * meet on devices[0] for the same ascending fold — results are bit-identical to one device and
+ * to n_gpus processes.  Exchange: NCCL communicators from ncclCommInitAll when the devices are
+ * distinct; peer copies (cudaMemcpyPeerAsync) when a device is listed twice or
+ * SSTAT_PEER_EXCHANGE=1.  Group calls:
+ *   sstat_cuda_dataset / _comoments / _column_sum: a FILE or HOST source is read by every member
+ *     (each its own ranges); a DEVICE source is an ARRAY of n_gpus sources, element i = member
+ *     i's shard on devices[i] (first_row / n_rows as in the multi-process call);
+ *   sstat_cuda_accumulate: the member whose device holds the chunk (host chunks: member 0);
+ *   sstat_cuda_range_partials: member 0;
+ *   sstat_cuda_generate: the member whose device holds dst;
+ *   sstat_cuda_set_staging / _set_host_threads: every member (host threads default to
+ *     min(16, cores) / n_gpus per member);
+ *   sstat_cuda_set_stream (non-NULL) and sstat_cuda_comm_init: rejected. */
+int sstat_cuda_init_devices(sstat_cuda_ctx** ctx, int n_gpus, const int* devices);
+/* Devices a context drives: 1, or the group's n_gpus. */
+int sstat_cuda_device_count(const sstat_cuda_ctx* ctx);
 int sstat_cuda_destroy(sstat_cuda_ctx* ctx);
 
 /* Launch work on an external cudaStream_t (e.g. the host framework's current stream);
- * NULL restores the context's own stream. */
+ * NULL restores the context's own stream.  The own stream is a blocking stream: it is ordered
+ * after work on the legacy default stream, so device sources written there need no sync. */
 int sstat_cuda_set_stream(sstat_cuda_ctx* ctx, void* cuda_stream);
 
 /* Host staging for HOST/FILE sources: `slots` device buffers of `slot_bytes` each. */
@@ -147,7 +183,10 @@ int sstat_cuda_set_staging(sstat_cuda_ctx* ctx, uint32_t slots, uint64_t slot_by
  * one core's copy rate.  0 = min(16, hardware threads).  Does not change any result. */
 int sstat_cuda_set_host_threads(sstat_cuda_ctx* ctx, uint32_t threads);
 
-/* ---- multi-GPU (one process per GPU, rows sharded contiguously by range) ---- */
+/* ---- multi-GPU (one process per GPU, rows sharded contiguously by range) ----
+ * A rank whose local phase fails still joins the exchange with its status in its header: every
+ * rank returns an error (the failing one its own, the others SSTAT_ERR_PEER), none hangs —
+ * except after a sticky CUDA error, which leaves the device unable to take part. */
 /* 128-byte ncclUniqueId, created on rank 0 and broadcast by the host framework. */
 int sstat_cuda_nccl_unique_id(void* id_out, size_t id_bytes);
 int sstat_cuda_comm_init(sstat_cuda_ctx* ctx, int rank, int world, const void* id, size_t id_bytes);
@@ -211,7 +250,7 @@ int sstat_cuda_comoments(sstat_cuda_ctx* ctx, const sstat_cuda_source* src, uint
 
 /* The range fold over gathered per-rank buffers (host memory), the same code the device
  * runs after the all-gather: rank q's buffer starts at buf + q*rank_stride with a
- * 4-double header, then its ranges [floor(qR/W), floor((q+1)R/W)) of p + p(p+1)/2
+ * 4-double header ({lowest failing range, first non-finite row*p+col, status, 0}), then its ranges [floor(qR/W), floor((q+1)R/W)) of p + p(p+1)/2
  * doubles each.  flags & SSTAT_FLAG_REFEXACT (or Binary32Diagnostic): the reference's
  * ascending fold from +0.0; otherwise the 8-lane fast fold of the default mode.
  * out receives p + p(p+1)/2 doubles. */

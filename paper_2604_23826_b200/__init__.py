@@ -19,6 +19,7 @@ from .sstat import (  # noqa: F401
     ReductionPlan,
     ReductionTimings,
     RowRange,
+    RowReader,
     SchemaMismatchError,
     SuffStats,
     accumulate_chunk,

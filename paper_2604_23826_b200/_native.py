@@ -25,10 +25,12 @@ ERR_OOM = 6
 ERR_UNSUPPORTED = 7
 ERR_IO = 8
 ERR_FORMAT = 9
+ERR_PEER = 10
 
 SRC_DEVICE = 0
 SRC_HOST = 1
 SRC_FILE = 2
+SRC_READER = 3
 
 FLAG_NO_SHIFT = 1 << 0
 FLAG_REFEXACT = 1 << 1
@@ -42,6 +44,8 @@ EXPORTS = (
     "sstat_cuda_abi_version",
     "sstat_status_string",
     "sstat_cuda_init",
+    "sstat_cuda_init_devices",
+    "sstat_cuda_device_count",
     "sstat_cuda_destroy",
     "sstat_cuda_set_stream",
     "sstat_cuda_set_staging",
@@ -89,6 +93,10 @@ class Timings(Structure):
     ]
 
 
+# sstat_read_rows_fn: (user, first_row, n_rows, scratch) -> rows pointer (NULL = failure)
+READ_ROWS_FN = ctypes.CFUNCTYPE(c_void_p, c_void_p, c_uint64, c_uint64, c_void_p)
+
+
 class Source(Structure):
     _fields_ = [
         ("kind", c_uint32),
@@ -97,6 +105,8 @@ class Source(Structure):
         ("first_row", c_uint64),
         ("n_rows", c_uint64),
         ("path", c_char_p),
+        ("read_rows", READ_ROWS_FN),
+        ("user", c_void_p),
     ]
 
 
@@ -133,6 +143,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "sstat_cuda_abi_version": (c_int, []),
         "sstat_status_string": (c_char_p, [c_int]),
         "sstat_cuda_init": (c_int, [P(c_void_p), c_int]),
+        "sstat_cuda_init_devices": (c_int, [P(c_void_p), c_int, P(c_int)]),
+        "sstat_cuda_device_count": (c_int, [c_void_p]),
         "sstat_cuda_destroy": (c_int, [c_void_p]),
         "sstat_cuda_set_stream": (c_int, [c_void_p, c_void_p]),
         "sstat_cuda_set_staging": (c_int, [c_void_p, c_uint32, c_uint64]),

@@ -36,6 +36,10 @@ struct TileJob {
     uint64_t tile_begin, tile_end; // tiles of this launch
     double* tile_partials;         // [n_tiles][partial_len(p)] canonical, shifted space
     unsigned long long* claim;     // 8-byte device scratch for K2's dynamic work split (or nullptr)
+    // K2's idle-slot launch: the caller context's own side stream and fork / join events
+    // (nullptr: no side launch, the clustered launch takes every tile)
+    cudaStream_t side;
+    cudaEvent_t fork, join;
 };
 
 // Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).

@@ -193,13 +193,17 @@ struct sstat_cuda_ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t own = nullptr, stream = nullptr, copy = nullptr;
+    // K2's idle-slot launch runs on this context's own side stream (TileJob::side)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::mutex mu;
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
-    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags, d_counts, d_aux, d_claim;
-    HostBuf h_meta, h_result, h_shift, h_flags, h_counts;
+    DevBuf d_meta, d_tiles, d_rank, d_gather, d_shift, d_result, d_flags, d_counts, d_aux, d_claim, d_pieces;
+    HostBuf h_meta, h_result, h_shift, h_flags, h_counts, h_pieces;
     uint32_t n_slots = 4;
-    uint64_t slot_bytes = 256ull << 20;
+    uint64_t slot_bytes = 256ull << 20;  // requested slot size
+    uint64_t slot_cap = 0;               // allocated: >= slot_bytes, grown to the largest unsplittable unit
     std::vector<DevBuf> slots;
     std::vector<HostBuf> bounce;
     std::vector<cudaEvent_t> ev_copied, ev_free;
@@ -220,6 +224,14 @@ struct sstat_cuda_ctx {
     cudaStream_t cap = nullptr;  // private capture stream (the caller's stream is never captured)
     cudaGraphExec_t graph = nullptr;
     std::vector<uint64_t> graph_key;
+    // ---- device group (sstat_cuda_init_devices): one process driving G devices ----
+    // members[g] is a full per-device context with rank g of world G; the group context itself
+    // owns no device state.  Exchange: NCCL (ncclCommInitAll over distinct devices) or peer
+    // copies into member 0 (`peer`: a device listed twice, or SSTAT_PEER_EXCHANGE=1).
+    std::vector<sstat_cuda_ctx*> members;
+    bool peer = false;
+    std::unique_ptr<FillPool> gpool;  // one host thread per member for the local phase
+    bool is_group() const { return !members.empty(); }
 };
 
 namespace {
@@ -349,10 +361,23 @@ struct HostRows {
     const double* host_row(uint64_t row) const {
         return static_cast<const double*>(src->ptr) + (row - src->first_row) * p;
     }
+    bool reader() const { return src->kind == SSTAT_SRC_READER; }
     // copy rows [row, row + n) into dst (pageable ptr / file)
     void fill(void* dst, uint64_t row, uint64_t n) const {
         if (file) read_exact(file->fd, dst, n * p * 8, 64 + row * p * 8);
         else std::memcpy(dst, host_row(row), n * p * 8);
+    }
+    // rows [row, row + n) in host memory: the reader's own pointer, or `scratch` once filled
+    const void* get(void* scratch, uint64_t row, uint64_t n) const {
+        if (!reader()) {
+            fill(scratch, row, n);
+            return scratch;
+        }
+        const void* q = src->read_rows(src->user, row, n, scratch);
+        if (!q)
+            throw Fail{SSTAT_ERR_IO, "read_rows failed for rows [" + std::to_string(row) + ", " +
+                                         std::to_string(row + n) + ")"};
+        return q;
     }
     // the same, as row blocks of >= 4 MiB spread over the feeder threads
     void fill_parallel(FillPool& pool, void* dst, uint64_t row, uint64_t n) const {
@@ -368,7 +393,11 @@ struct HostRows {
     }
 };
 
-void ensure_slots(sstat_cuda_ctx* c, bool need_bounce) {
+// Staging ring of n_slots device slots (+ pinned bounce buffers for pageable / file sources).
+// Slots are at least the requested slot_bytes and at least `min_bytes`: the largest unit the
+// call cannot split (a fast-path tile; reference-order ranges are split into pieces instead).
+void ensure_slots(sstat_cuda_ctx* c, bool need_bounce, uint64_t min_bytes) {
+    const uint64_t cap = std::max<uint64_t>(c->slot_bytes, (min_bytes + 127) & ~(uint64_t)127);
     if (c->slots.size() != c->n_slots) {
         for (auto& s : c->slots) s.release();
         for (auto& b : c->bounce) b.release();
@@ -384,9 +413,10 @@ void ensure_slots(sstat_cuda_ctx* c, bool need_bounce) {
         }
     }
     for (uint32_t i = 0; i < c->n_slots; ++i) {
-        CUDA_TRY(c->slots[i].reserve(c->slot_bytes));
-        if (need_bounce) CUDA_TRY(c->bounce[i].reserve(c->slot_bytes));
+        CUDA_TRY(c->slots[i].reserve(cap));
+        if (need_bounce) CUDA_TRY(c->bounce[i].reserve(cap));
     }
+    c->slot_cap = cap;
 }
 
 enum class Mode { Dataset, Chunk, Partials, Comoments };
@@ -406,13 +436,19 @@ uint64_t tile_rows_for(uint32_t p) { return p > 64 ? widep_tile_rows(p) : kTileR
 
 struct Outcome {
     uint64_t bad_lin = kNone;  // lowest first-non-finite linear index over all ranks
+    int failed_rank = -1;      // first rank whose header reports a failure (multi-process)
+    int failed_status = 0;
 };
 
-// Streams the rows of tiles [t0, t1) (or whole ranges for refexact) through the staging ring.
-// `launch(base, base_row, first_tile, last_tile)` enqueues the kernel for one chunk.
+// Streams units of rows (tiles, or reference-order range pieces) through the staging ring.
+// `launch(base, base_row, first_unit, last_unit)` enqueues the kernel for one chunk: a maximal
+// run of row-contiguous units fitting one slot.  A unit with chained[u] != 0 (a later piece of a
+// range streamed in pieces) always starts a new chunk, so only a chunk's first unit continues
+// an earlier one.
 template <class Launch>
 void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint64_t>& unit_row,
-                   const std::vector<uint64_t>& unit_rows, Launch&& launch, sstat_cuda_timings* tm) {
+                   const std::vector<uint64_t>& unit_rows, Launch&& launch, sstat_cuda_timings* tm,
+                   const std::vector<uint8_t>* chained = nullptr) {
     const uint64_t row_bytes = (uint64_t)hr.p * 8;
     const uint64_t n_units = unit_row.size();
     uint64_t u = 0, chunk = 0;
@@ -421,8 +457,10 @@ void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint
         uint64_t v = u, bytes = 0;
         while (v < n_units) {
             const uint64_t b = unit_rows[v] * row_bytes;
-            if (v > u && (bytes + b > c->slot_bytes || unit_row[v] != unit_row[v - 1] + unit_rows[v - 1])) break;
-            if (b > c->slot_bytes) throw Fail{SSTAT_ERR_UNSUPPORTED, "staging slot smaller than one work unit"};
+            if (v > u && (bytes + b > c->slot_cap || unit_row[v] != unit_row[v - 1] + unit_rows[v - 1] ||
+                          (chained && (*chained)[v])))
+                break;
+            if (b > c->slot_cap) throw Fail{SSTAT_ERR_UNSUPPORTED, "staging slot smaller than one work unit"};
             bytes += b;
             ++v;
         }
@@ -435,9 +473,13 @@ void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint
         } else {
             // the bounce buffer of this slot is reused: its previous copy must be done
             if (chunk >= c->n_slots) CUDA_TRY(cudaEventSynchronize(c->ev_copied[slot]));
-            if (!c->pool) c->pool.reset(new FillPool(c->host_threads ? c->host_threads : default_host_threads()));
-            hr.fill_parallel(*c->pool, c->bounce[slot].p, row0, nrows);
-            host_src = c->bounce[slot].p;
+            if (hr.reader()) {
+                host_src = hr.get(c->bounce[slot].p, row0, nrows);
+            } else {
+                if (!c->pool) c->pool.reset(new FillPool(c->host_threads ? c->host_threads : default_host_threads()));
+                hr.fill_parallel(*c->pool, c->bounce[slot].p, row0, nrows);
+                host_src = c->bounce[slot].p;
+            }
         }
         CUDA_TRY(cudaMemcpyAsync(c->slots[slot].p, host_src, bytes, cudaMemcpyHostToDevice, c->copy));
         CUDA_TRY(cudaEventRecord(c->ev_copied[slot], c->copy));
@@ -491,9 +533,9 @@ void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFil
             f.range = 0;
             throw f;
         }
-    } else if (src->kind == SSTAT_SRC_DEVICE || src->kind == SSTAT_SRC_HOST) {
-        if (!src->ptr && P.total > 0) {
-            inv.msg = "null row pointer";
+    } else if (src->kind == SSTAT_SRC_DEVICE || src->kind == SSTAT_SRC_HOST || src->kind == SSTAT_SRC_READER) {
+        if (src->kind == SSTAT_SRC_READER ? !src->read_rows : (!src->ptr && P.total > 0)) {
+            inv.msg = src->kind == SSTAT_SRC_READER ? "null read_rows callback" : "null row pointer";
             throw inv;
         }
         if (world == 1 && whole) {
@@ -584,21 +626,85 @@ bool rows_aligned16(const double* base, uint64_t base_row, const uint64_t* start
     return true;
 }
 
-// The engine proper.  Returns the all-rank outcome; throws Fail.
-void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
-         sstat_cuda_timings* tm) {
-    BinFile file;
-    Trace trace_run(P.mode == Mode::Comoments ? "sstat.comoments" : P.mode == Mode::Partials ? "sstat.range_partials"
-                    : P.mode == Mode::Chunk ? "sstat.accumulate_chunk" : "sstat.dataset");
+// What the local phase hands to the exchange and fold.  refexact / comoments are pure functions
+// of the arguments (classify), so a rank that failed early still knows its layout.
+struct Local {
+    bool refexact = false, comoments = false, shift = false;
+    bool graphable = false;  // one GPU, resident K1 pass: folds and read-back are in the graph
+    bool scanned = false;    // the non-finite scan already ran for this rank
+    double* rank_buf = nullptr;
+    uint64_t rank_stride = 0;  // kHdr + lmax * E doubles
+};
+
+void classify(const Plan& P, Local& st) {
+    st.comoments = P.mode == Mode::Comoments;  // co-moments always take the shifted fast path
+    st.refexact = !st.comoments && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1);
+    st.shift = !(P.flags & SSTAT_FLAG_NO_SHIFT) && !st.refexact;
+}
+
+int call_world(const sstat_cuda_ctx* c, const Plan& P) {
+    return (P.mode == Mode::Dataset || P.mode == Mode::Comoments) ? c->world : 1;
+}
+
+// Reference-order pieces: each local range split into pieces of at most `max_rows` rows (an
+// even number, so a piece keeps its range's 16-byte alignment); piece_range = its local range,
+// chained = a later piece (its chains continue the earlier pieces').
+struct Pieces {
+    std::vector<uint64_t> row, rows, range;
+    std::vector<uint8_t> chained;
+};
+Pieces split_ranges(const Plan& P, uint64_t max_rows) {
+    Pieces pc;
+    max_rows = std::max<uint64_t>(2, max_rows & ~(uint64_t)1);
+    for (uint64_t i = 0; i < P.L; ++i) {
+        const uint64_t rs = P.starts[P.r0 + i], rc = P.counts[P.r0 + i];
+        uint64_t off = 0;
+        do {
+            const uint64_t k = std::min(max_rows, rc - off);
+            pc.row.push_back(rs + off);
+            pc.rows.push_back(k);
+            pc.range.push_back(i);
+            pc.chained.push_back(off > 0);
+            off += k;
+        } while (off < rc);
+    }
+    return pc;
+}
+
+// Pieces' (start, count) to the device: [starts | counts] of n pieces.
+uint64_t* upload_pieces(sstat_cuda_ctx* c, const Pieces& pc, cudaStream_t s) {
+    const uint64_t n = pc.row.size();
+    CUDA_TRY(c->h_pieces.reserve(2 * n * 8));
+    CUDA_TRY(c->d_pieces.reserve(2 * n * 8));
+    uint64_t* h = c->h_pieces.as<uint64_t>();
+    std::copy(pc.row.begin(), pc.row.end(), h);
+    std::copy(pc.rows.begin(), pc.rows.end(), h + n);
+    CUDA_TRY(cudaMemcpyAsync(c->d_pieces.p, h, 2 * n * 8, cudaMemcpyHostToDevice, s));
+    return c->d_pieces.as<uint64_t>();
+}
+
+bool host_pinned(const sstat_cuda_source* src) {
+    if (src->kind != SSTAT_SRC_HOST) return false;
+    cudaPointerAttributes attr{};
+    bool pinned = false;
+    if (cudaPointerGetAttributes(&attr, src->ptr) == cudaSuccess) pinned = attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return pinned;
+}
+
+// Phase 1: this device's ranges — accumulate (K1/K1w/K2 or reference order), fold per range
+// (K3a) into the rank buffer [header | lmax x E], and (world > 1) locate the first non-finite
+// value so every rank knows it before the exchange.  One GPU, resident K1: the whole pass
+// including the folds and the read-back is one replayed CUDA graph.
+void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile& file, Local& st,
+               sstat_cuda_timings* tm) {
     check_plan(c, src, P, file);
-    const int world = (P.mode == Mode::Dataset || P.mode == Mode::Comoments) ? c->world : 1;
-    const bool comoments = P.mode == Mode::Comoments;  // co-moments always take the shifted fast path
-    const bool refexact = !comoments && ((P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1);
+    const int world = call_world(c, P);
+    const bool comoments = st.comoments, refexact = st.refexact, shift = st.shift;
     // K2 stages at least one k-step (4 rows) of every column in shared memory, double-buffered
     if (P.p > kMaxWideP && !refexact)
         throw Fail{SSTAT_ERR_UNSUPPORTED, "p = " + std::to_string(P.p) + " exceeds the " + std::to_string(kMaxWideP) +
                                               "-column limit of the fast path (reference-order mode has none)"};
-    const bool shift = !(P.flags & SSTAT_FLAG_NO_SHIFT) && !refexact;
     const uint32_t p = P.p;
     const uint64_t E = P.E, L = P.L;
     cudaStream_t s = c->stream;
@@ -614,10 +720,14 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     const uint64_t rank_stride = kHdr + P.lmax * E;
     CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
     CUDA_TRY(c->d_flags.reserve(std::max<uint64_t>(L, 1) * 4));
-    // the header (lowest failing range, first non-finite index) and the range flags are only
-    // written when something is flagged: reset them only after such a call or a realloc
+    st.rank_stride = rank_stride;
+    st.rank_buf = c->d_rank.as<double>();
+    // the header ([0] lowest failing range, [1] first non-finite index: all-ones = none;
+    // [2] the rank's status, [3] spare: 0) and the range flags are only written when something
+    // is flagged or failed: reset them only after such a call or a realloc
     if (!(c->flags_clean && c->clean_rank == c->d_rank.gen && c->clean_flags == c->d_flags.gen && L <= c->clean_len)) {
-        CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, kHdr * 8, s));
+        CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, 2 * 8, s));
+        CUDA_TRY(cudaMemsetAsync(c->d_rank.as<double>() + 2, 0, (kHdr - 2) * 8, s));
         CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
         c->clean_rank = c->d_rank.gen;
         c->clean_flags = c->d_flags.gen;
@@ -653,6 +763,9 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
         if (wide) {
             CUDA_TRY(c->d_claim.reserve(sizeof(unsigned long long)));
             j.claim = c->d_claim.as<unsigned long long>();
+            j.side = c->side;
+            j.fork = c->ev_fork;
+            j.join = c->ev_join;
         }
         uint32_t kernels = 1;
         CUDA_TRY(wide ? (splitp_handles(p) ? launch_splitp(j, c->sms, s) : launch_widep(j, c->sms, s, &kernels))
@@ -667,6 +780,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     // together — five events measured 14 us slower per call at C1 and C2)
     const bool graphable = src->kind == SSTAT_SRC_DEVICE && world == 1 && P.mode == Mode::Dataset && !refexact &&
                            !wide && L > 0 && nt > 0 && !getenv("SSTAT_NO_GRAPH");
+    st.graphable = graphable;
     if (graphable) {
         CUDA_TRY(c->h_result.reserve(E * 8 + kHdr * 8));
         CUDA_TRY(c->d_result.reserve((E + kHdr) * 8));  // K3b appends the rank header
@@ -725,19 +839,18 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
             tm->kernel_launches += shift ? 4 : 3;
         }
+        return;  // everything up to the read-back is in the graph
     }
 
-    if (!graphable) CUDA_TRY(cudaEventRecord(c->ev[0], s));
-    if (!graphable && tm) tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
-    bool scanned = false;  // the non-finite scan already ran for this rank
-    if (graphable) {
-        // everything up to the read-back is in the graph
-    } else if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
+    CUDA_TRY(cudaEventRecord(c->ev[0], s));
+    if (tm) tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
+    if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
         const double* base = static_cast<const double*>(src->ptr);
         const uint64_t base_row = src->first_row;
         if (refexact) {
             CUDA_TRY(launch_refexact(base, base_row, d_starts, d_counts, (uint32_t)L, p, P.precision, P.r0, rank_buf,
-                                     rank_buf + kHdr, d_flags, rows_aligned16(base, base_row, P.starts + P.r0, L, p), s));
+                                     rank_buf + kHdr, d_flags, rows_aligned16(base, base_row, P.starts + P.r0, L, p),
+                                     false, s));
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
             if (tm) tm->kernel_launches += 1;
         } else {
@@ -763,49 +876,47 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
             CUDA_TRY(launch_find_nonfinite(base, base_row, d_starts, d_counts, (uint32_t)L, p, d_flags, rank_buf,
                                            c->sms * 2, s));
             if (tm) tm->kernel_launches += 1;
-            scanned = true;
+            st.scanned = true;
         }
         CUDA_TRY(cudaEventRecord(c->ev[2], s));
     } else if (L > 0) {
         // ---- host / file source: pinned staging ring, copy stream || compute stream ----
-        cudaPointerAttributes attr{};
-        bool pinned = false;
-        if (src->kind == SSTAT_SRC_HOST) {
-            if (cudaPointerGetAttributes(&attr, src->ptr) == cudaSuccess)
-                pinned = attr.type == cudaMemoryTypeHost;
-            cudaGetLastError();
-        }
+        const bool pinned = host_pinned(src);
         HostRows hr{src, src->kind == SSTAT_SRC_FILE ? &file : nullptr, p, pinned};
-        ensure_slots(c, !pinned);
+        // reference-order ranges stream as slot-sized pieces; fast-path tiles are whole units
+        ensure_slots(c, !pinned, refexact ? 2ull * p * 8 : TR * p * 8);  // (readers: bounce = scratch)
         if (shift) {
             CUDA_TRY(c->h_shift.reserve(L * p * 8));
             double* hs = c->h_shift.as<double>();
             for (uint64_t i = 0; i < L; ++i) {
                 if (P.counts[P.r0 + i] == 0) std::fill(hs + i * p, hs + (i + 1) * p, 0.0);
                 else if (file.fd >= 0) hr.fill(hs + i * p, P.starts[P.r0 + i], 1);
-                else std::memcpy(hs + i * p, hr.host_row(P.starts[P.r0 + i]), p * 8);
+                else if (hr.reader()) {
+                    const void* q = hr.get(hs + i * p, P.starts[P.r0 + i], 1);
+                    if (q != hs + i * p) std::memcpy(hs + i * p, q, p * 8);
+                } else std::memcpy(hs + i * p, hr.host_row(P.starts[P.r0 + i]), p * 8);
             }
             CUDA_TRY(cudaMemcpyAsync(c->d_shift.p, hs, L * p * 8, cudaMemcpyHostToDevice, s));
         }
         CUDA_TRY(cudaEventRecord(c->ev[0], s));
         CUDA_TRY(cudaStreamWaitEvent(c->copy, c->ev[0], 0));
         if (refexact) {
-            // units = whole ranges; each chunk launches the sequential chains of its ranges
-            std::vector<uint64_t> urow(L), urows(L);
-            for (uint64_t i = 0; i < L; ++i) {
-                urow[i] = P.starts[P.r0 + i];
-                urows[i] = P.counts[P.r0 + i];
-            }
-            stream_chunks(c, hr, urow, urows,
+            // units = range pieces of at most one slot; a range longer than a slot continues its
+            // chains across launches (resume_first), so the order of operations is unchanged
+            const Pieces pc = split_ranges(P, c->slot_cap / ((uint64_t)p * 8));
+            const uint64_t* d_pc = upload_pieces(c, pc, s);
+            const uint64_t npc = pc.row.size();
+            stream_chunks(c, hr, pc.row, pc.rows,
                           [&](const double* base, uint64_t base_row, uint64_t u0, uint64_t u1) {
-                              // ranges [u0, u1) of this chunk → partial slots u0 .. u1-1
-                              CUDA_TRY(launch_refexact(base, base_row, d_starts + u0, d_counts + u0, (uint32_t)(u1 - u0),
-                                                       p, P.precision, P.r0 + u0, rank_buf, rank_buf + kHdr + u0 * E,
-                                                       d_flags + u0,
-                                                       rows_aligned16(base, base_row, P.starts + P.r0 + u0, u1 - u0, p),
-                                                       s));
+                              // pieces [u0, u1) belong to consecutive local ranges from pc.range[u0]
+                              const uint64_t lr = pc.range[u0];
+                              CUDA_TRY(launch_refexact(base, base_row, d_pc + u0, d_pc + npc + u0, (uint32_t)(u1 - u0),
+                                                       p, P.precision, P.r0 + lr, rank_buf, rank_buf + kHdr + lr * E,
+                                                       d_flags + lr,
+                                                       rows_aligned16(base, base_row, pc.row.data() + u0, u1 - u0, p),
+                                                       pc.chained[u0] != 0, s));
                           },
-                          tm);
+                          tm, &pc.chained);
             CUDA_TRY(cudaEventRecord(c->ev[1], s));
         } else {
             std::vector<uint64_t> trow(nt), trows(nt);
@@ -848,7 +959,7 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                 std::vector<uint64_t> urow{P.starts[P.r0 + i]}, urows{P.counts[P.r0 + i]};
                 // split the range into slot-sized pieces of whole rows
                 std::vector<uint64_t> prow, prows;
-                const uint64_t per = std::max<uint64_t>(1, c->slot_bytes / (p * 8));
+                const uint64_t per = std::max<uint64_t>(1, c->slot_cap / (p * 8));
                 for (uint64_t r = 0; r < urows[0]; r += per) {
                     prow.push_back(urow[0] + r);
                     prows.push_back(std::min(per, urows[0] - r));
@@ -869,79 +980,98 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
                               nullptr);
             }
         }
-        scanned = true;
+        st.scanned = true;
         CUDA_TRY(cudaEventRecord(c->ev[2], s));
     } else {
         CUDA_TRY(cudaEventRecord(c->ev[1], s));
         CUDA_TRY(cudaEventRecord(c->ev[2], s));
     }
+}
 
-    if (P.mode == Mode::Partials) {
-        CUDA_TRY(c->h_result.reserve((L * E + kHdr) * 8));
-        double* hres = c->h_result.as<double>();
-        CUDA_TRY(cudaMemcpyAsync(hres, rank_buf, (kHdr + L * E) * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        std::memcpy(&out.bad_lin, hres + 1, 8);
-        if (L) std::memcpy(P.partials_host, hres + kHdr, L * E * 8);
-        return;
-    }
+// A rank whose local phase failed still joins the exchange: its header carries the status so
+// every rank fails together instead of waiting in the collective (reduce.hpp:111-134 never
+// deadlocks either).  The layout is a function of the arguments alone.
+void publish_status(sstat_cuda_ctx* c, const Plan& P, Local& st, int status) {
+    const uint64_t E = partial_len(P.p), lmax = (P.R + c->world - 1) / c->world;
+    st.rank_stride = kHdr + lmax * E;
+    CUDA_TRY(c->d_rank.reserve(st.rank_stride * 8));
+    st.rank_buf = c->d_rank.as<double>();
+    st.graphable = false;
+    const uint64_t hdr[kHdr] = {kNone, kNone, (uint64_t)status, 0};
+    CUDA_TRY(cudaMemcpyAsync(st.rank_buf, hdr, sizeof hdr, cudaMemcpyHostToDevice, c->stream));
+    c->flags_clean = false;
+}
 
-    // ---- exchange (rank-ordered all-gather of per-range partials) ----
-    Trace trace_tail("sstat.exchange+fold+readback");
-    const double* fold_buf = rank_buf;
-    if (graphable) {
-        // folds and read-back are in the graph
-    } else {
-    if (world > 1) {
-        CUDA_TRY(c->d_gather.reserve(rank_stride * world * 8));
-        ncclResult_t r = ncclAllGather(rank_buf, c->d_gather.p, rank_stride, ncclDouble, c->comm, s);
-        if (r != ncclSuccess) throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r)};
-        fold_buf = c->d_gather.as<double>();
-    }
-    CUDA_TRY(cudaEventRecord(c->ev[3], s));
-    CUDA_TRY(c->d_result.reserve((E + world * kHdr) * 8));
-    if (comoments) {
-        // every range's count (the merge weights), for all ranks' ranges
-        CUDA_TRY(c->h_counts.reserve(std::max<uint64_t>(P.R, 1) * 8));
-        CUDA_TRY(c->d_counts.reserve(std::max<uint64_t>(P.R, 1) * 8));
-        std::memcpy(c->h_counts.p, P.counts, P.R * 8);
-        CUDA_TRY(cudaMemcpyAsync(c->d_counts.p, c->h_counts.p, P.R * 8, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(launch_comoment_merge(fold_buf, rank_stride, P.R, world, c->d_counts.as<uint64_t>(), p,
-                                       c->d_result.as<double>(), s));
-    } else {
-        CUDA_TRY(launch_final_fold(fold_buf, rank_stride, P.R, world, p, refexact ? P.precision : 0u, refexact,
-                                   c->d_result.as<double>(), s));
-    }
-    if (tm) tm->kernel_launches += 1;
-    CUDA_TRY(cudaEventRecord(c->ev[4], s));
-    CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
-    // result and every rank's header in one read-back (K3b appends the headers)
-    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + world * kHdr) * 8, cudaMemcpyDeviceToHost, s));
+// Rank-ordered all-gather of the per-range partials (multi-process: one communicator rank per
+// process).  Returns the buffer the fold reads.
+const double* exchange(sstat_cuda_ctx* c, const Local& st, int world) {
+    if (world == 1) return st.rank_buf;
+    CUDA_TRY(c->d_gather.reserve(st.rank_stride * world * 8));
+    ncclResult_t r = ncclAllGather(st.rank_buf, c->d_gather.p, st.rank_stride, ncclDouble, c->comm, c->stream);
+    if (r != ncclSuccess) throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r)};
+    return c->d_gather.as<double>();
+}
+
+// Phase 2: the ascending range fold (K3b) or the co-moment merge over the gathered rank
+// buffers, one read-back of the result and every rank header, then the headers: lowest failing
+// range / first non-finite index over all ranks, and the first rank that reported a failure.
+void run_fold(sstat_cuda_ctx* c, const sstat_cuda_source* src, const Plan& P, const Local& st, const double* fold_buf,
+              int world, double* result_host, Outcome& out, sstat_cuda_timings* tm) {
+    Trace trace_tail("sstat.fold+readback");
+    const uint32_t p = P.p;
+    const uint64_t E = P.E ? P.E : partial_len(p), L = P.L;
+    cudaStream_t s = c->stream;
+    if (!st.graphable) {
+        CUDA_TRY(cudaEventRecord(c->ev[3], s));
+        CUDA_TRY(c->d_result.reserve((E + world * kHdr) * 8));
+        if (st.comoments) {
+            // every range's count (the merge weights), for all ranks' ranges
+            CUDA_TRY(c->h_counts.reserve(std::max<uint64_t>(P.R, 1) * 8));
+            CUDA_TRY(c->d_counts.reserve(std::max<uint64_t>(P.R, 1) * 8));
+            std::memcpy(c->h_counts.p, P.counts, P.R * 8);
+            CUDA_TRY(cudaMemcpyAsync(c->d_counts.p, c->h_counts.p, P.R * 8, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(launch_comoment_merge(fold_buf, st.rank_stride, P.R, world, c->d_counts.as<uint64_t>(), p,
+                                           c->d_result.as<double>(), s));
+        } else {
+            CUDA_TRY(launch_final_fold(fold_buf, st.rank_stride, P.R, world, p, st.refexact ? P.precision : 0u,
+                                       st.refexact, c->d_result.as<double>(), s));
+        }
+        if (tm) tm->kernel_launches += 1;
+        CUDA_TRY(cudaEventRecord(c->ev[4], s));
+        CUDA_TRY(c->h_result.reserve(E * 8 + world * kHdr * 8));
+        // result and every rank's header in one read-back (K3b appends the headers)
+        CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + world * kHdr) * 8, cudaMemcpyDeviceToHost, s));
     }
     double* hres = c->h_result.as<double>();
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
-    if (!scanned && world == 1 && L > 0) {
+    if (!st.scanned && world == 1 && L > 0) {
         uint64_t flagged;
         std::memcpy(&flagged, hres + E, 8);
         if (flagged != kNone) {  // error path: locate the first non-finite value of the flagged ranges
-            CUDA_TRY(launch_find_nonfinite(static_cast<const double*>(src->ptr), src->first_row, d_starts, d_counts,
-                                           (uint32_t)L, p, d_flags, rank_buf, c->sms * 2, s));
-            CUDA_TRY(cudaMemcpyAsync(hres + E, rank_buf, kHdr * 8, cudaMemcpyDeviceToHost, s));
+            uint64_t* d_starts = c->d_meta.as<uint64_t>();
+            CUDA_TRY(launch_find_nonfinite(static_cast<const double*>(src->ptr), src->first_row, d_starts, d_starts + L,
+                                           (uint32_t)L, p, c->d_flags.as<uint32_t>(), st.rank_buf, c->sms * 2, s));
+            CUDA_TRY(cudaMemcpyAsync(hres + E, st.rank_buf, kHdr * 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
         }
     }
     bool any_flag = false;
     for (int q = 0; q < world; ++q) {
-        uint64_t lin, range;
+        uint64_t lin, range, status;
         std::memcpy(&range, hres + E + q * kHdr, 8);
         std::memcpy(&lin, hres + E + q * kHdr + 1, 8);
+        std::memcpy(&status, hres + E + q * kHdr + 2, 8);
         out.bad_lin = std::min(out.bad_lin, lin);
-        any_flag |= range != kNone;
+        any_flag |= range != kNone || status != 0;
+        if (status != 0 && out.failed_rank < 0) {
+            out.failed_rank = q;
+            out.failed_status = (int)status;
+        }
     }
     c->flags_clean = !any_flag;
-    std::memcpy(result_host, hres, E * 8);
-    if (tm && graphable) {  // the graph records three events: K1, then both folds together
+    if (result_host) std::memcpy(result_host, hres, E * 8);
+    if (tm && st.graphable) {  // the graph records three events: K1, then both folds together
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
         tm->kernel_seconds += ms * 1e-3;
@@ -962,21 +1092,77 @@ void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* resul
     }
 }
 
+Fail peer_failure(const Outcome& o) {
+    return Fail{SSTAT_ERR_PEER, "rank " + std::to_string(o.failed_rank) + " failed: " +
+                                    sstat_status_string(o.failed_status)};
+}
+
+// The engine proper on one context (one GPU, or one rank of a multi-process communicator).
+// Returns the all-rank outcome; throws Fail.
+void run(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, double* result_host, Outcome& out,
+         sstat_cuda_timings* tm) {
+    BinFile file;
+    Trace trace_run(P.mode == Mode::Comoments ? "sstat.comoments" : P.mode == Mode::Partials ? "sstat.range_partials"
+                    : P.mode == Mode::Chunk ? "sstat.accumulate_chunk" : "sstat.dataset");
+    Local st;
+    classify(P, st);
+    const int world = call_world(c, P);
+    if (world == 1) {
+        run_local(c, src, P, file, st, tm);
+        if (P.mode == Mode::Partials) {
+            const uint64_t E = P.E, L = P.L;
+            CUDA_TRY(c->h_result.reserve((L * E + kHdr) * 8));
+            double* hres = c->h_result.as<double>();
+            CUDA_TRY(cudaMemcpyAsync(hres, st.rank_buf, (kHdr + L * E) * 8, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            std::memcpy(&out.bad_lin, hres + 1, 8);
+            if (L) std::memcpy(P.partials_host, hres + kHdr, L * E * 8);
+            return;
+        }
+        run_fold(c, src, P, st, st.rank_buf, 1, result_host, out, tm);
+        return;
+    }
+    // multi-process: a local failure is published in the rank header, the exchange still runs
+    Fail local;
+    bool failed = false;
+    try {
+        run_local(c, src, P, file, st, tm);
+    } catch (const Fail& f) {
+        local = f;
+        failed = true;
+    }
+    if (failed) {
+        try {
+            publish_status(c, P, st, local.status);
+        } catch (const Fail&) {
+            throw local;  // the device cannot even publish (sticky CUDA error): peers are not told
+        }
+    }
+    const double* fold_buf = exchange(c, st, world);
+    run_fold(c, src, P, st, fold_buf, world, result_host, out, tm);
+    if (failed) throw local;
+    if (out.failed_rank >= 0) throw peer_failure(out);
+}
+
 // column_sum (reference src/reduce.cpp:32-88) over the plan's ranges; 32-byte partials
-// {float sum, exact lo, exact hi, first non-integral row} per tile / range.
+// {float sum, exact lo, exact hi, first non-integral row} per tile / range.  The rank buffer is
+// [header part {0, status, 0, 0} | lmax range parts].
 struct ColResult {
     double f;
     uint64_t lo, hi, bad_row;
 };
 
-void run_colsum(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32_t column, ColResult& res) {
-    Trace trace_run("sstat.column_sum");
-    BinFile file;
+struct ColLocal {
+    char* rank_buf = nullptr;
+    uint64_t stride = 0;  // in 32-byte parts: header + lmax
+};
+
+void colsum_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32_t column, BinFile& file,
+                  ColLocal& cl) {
     check_plan(c, src, P, file);
     if (column >= P.p)
         throw Fail{SSTAT_ERR_INVALID, "column_sum: column " + std::to_string(column) + " out of range, dataset has " +
                                           std::to_string(P.p) + " columns"};
-    const int world = c->world;
     const uint32_t p = P.p;
     const uint64_t L = P.L;
     const bool sequential = (P.flags & SSTAT_FLAG_REFEXACT) || P.precision == 1;
@@ -985,42 +1171,39 @@ void run_colsum(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32
     uint64_t* d_counts = d_starts + L;
     uint64_t* d_prefix = d_starts + 2 * L;
     const uint64_t nt = P.n_tiles;
-    const uint64_t stride = 1 + P.lmax;  // in 32-byte partials: header slot + ranges
-    CUDA_TRY(c->d_rank.reserve(stride * 32));
+    cl.stride = 1 + P.lmax;
+    CUDA_TRY(c->d_rank.reserve(cl.stride * 32));
     CUDA_TRY(c->d_aux.reserve(std::max<uint64_t>(nt, 1) * 32));
-    char* rank_buf = static_cast<char*>(c->d_rank.p);
-    void* range_parts = rank_buf + 32;
+    cl.rank_buf = static_cast<char*>(c->d_rank.p);
+    CUDA_TRY(cudaMemsetAsync(cl.rank_buf, 0, 32, s));  // header part: status 0
+    void* range_parts = cl.rank_buf + 32;
     if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
         const double* base = static_cast<const double*>(src->ptr);
         CUDA_TRY(launch_colsum(base, src->first_row, p, column, d_starts, d_counts, d_prefix, (uint32_t)L, 0, nt,
-                               sequential, P.precision, c->d_aux.p, range_parts, c->sms, s));
+                               sequential, P.precision, c->d_aux.p, range_parts, c->sms, false, s));
         if (!sequential) CUDA_TRY(launch_colsum_range_fold(c->d_aux.p, d_prefix, (uint32_t)L, range_parts, s));
     } else if (L > 0) {
-        cudaPointerAttributes attr{};
-        bool pinned = false;
-        if (src->kind == SSTAT_SRC_HOST) {
-            if (cudaPointerGetAttributes(&attr, src->ptr) == cudaSuccess) pinned = attr.type == cudaMemoryTypeHost;
-            cudaGetLastError();
-        }
+        const bool pinned = host_pinned(src);
         HostRows hr{src, src->kind == SSTAT_SRC_FILE ? &file : nullptr, p, pinned};
-        ensure_slots(c, !pinned);
+        ensure_slots(c, !pinned, sequential ? 2ull * p * 8 : (uint64_t)kTileRows * p * 8);
         cudaEvent_t e0 = c->ev[0];
         CUDA_TRY(cudaEventRecord(e0, s));
         CUDA_TRY(cudaStreamWaitEvent(c->copy, e0, 0));
-        std::vector<uint64_t> urow, urows;
-        if (sequential) {  // units = whole ranges
-            for (uint64_t i = 0; i < L; ++i) {
-                urow.push_back(P.starts[P.r0 + i]);
-                urows.push_back(P.counts[P.r0 + i]);
-            }
-            stream_chunks(c, hr, urow, urows,
+        if (sequential) {  // units = range pieces; a piece after the first continues its range's sums
+            const Pieces pc = split_ranges(P, c->slot_cap / ((uint64_t)p * 8));
+            const uint64_t* d_pc = upload_pieces(c, pc, s);
+            const uint64_t npc = pc.row.size();
+            stream_chunks(c, hr, pc.row, pc.rows,
                           [&](const double* base, uint64_t base_row, uint64_t u0, uint64_t u1) {
-                              CUDA_TRY(launch_colsum(base, base_row, p, column, d_starts + u0, d_counts + u0, nullptr,
+                              const uint64_t lr = pc.range[u0];
+                              CUDA_TRY(launch_colsum(base, base_row, p, column, d_pc + u0, d_pc + npc + u0, nullptr,
                                                      (uint32_t)(u1 - u0), 0, 0, true, P.precision, nullptr,
-                                                     static_cast<char*>(range_parts) + 32 * u0, c->sms, s));
+                                                     static_cast<char*>(range_parts) + 32 * lr, c->sms,
+                                                     pc.chained[u0] != 0, s));
                           },
-                          nullptr);
+                          nullptr, &pc.chained);
         } else {  // units = tiles
+            std::vector<uint64_t> urow, urows;
             for (uint64_t i = 0; i < L; ++i) {
                 const uint64_t rs = P.starts[P.r0 + i], rc = P.counts[P.r0 + i];
                 for (uint64_t q = 0; q * kTileRows < rc; ++q) {
@@ -1032,25 +1215,261 @@ void run_colsum(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32
                           [&](const double* base, uint64_t base_row, uint64_t t0, uint64_t t1) {
                               CUDA_TRY(launch_colsum(base, base_row, p, column, d_starts, d_counts, d_prefix,
                                                      (uint32_t)L, t0, t1, false, P.precision, c->d_aux.p, nullptr,
-                                                     c->sms, s));
+                                                     c->sms, false, s));
                           },
                           nullptr);
             CUDA_TRY(launch_colsum_range_fold(c->d_aux.p, d_prefix, (uint32_t)L, range_parts, s));
         }
     }
-    const void* fold_buf = rank_buf;
-    if (world > 1) {
-        CUDA_TRY(c->d_gather.reserve(stride * 32 * world));
-        ncclResult_t r = ncclAllGather(rank_buf, c->d_gather.p, stride * 4, ncclDouble, c->comm, s);
-        if (r != ncclSuccess) throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r)};
-        fold_buf = c->d_gather.p;
-    }
-    CUDA_TRY(c->d_result.reserve(64));
+}
+
+void colsum_publish(sstat_cuda_ctx* c, const Plan& P, ColLocal& cl, int status) {
+    cl.stride = 1 + (P.R + c->world - 1) / c->world;
+    CUDA_TRY(c->d_rank.reserve(cl.stride * 32));
+    cl.rank_buf = static_cast<char*>(c->d_rank.p);
+    const uint64_t hdr[4] = {0, (uint64_t)status, 0, 0};
+    CUDA_TRY(cudaMemcpyAsync(cl.rank_buf, hdr, sizeof hdr, cudaMemcpyHostToDevice, c->stream));
+}
+
+// The final ascending fold over the gathered rank buffers, and every rank's header part.
+void colsum_fold(sstat_cuda_ctx* c, const Plan& P, const void* fold_buf, uint64_t stride, int world, ColResult& res,
+                 Outcome& out) {
+    cudaStream_t s = c->stream;
+    CUDA_TRY(c->d_result.reserve((1 + world) * 32));
     CUDA_TRY(launch_colsum_final(fold_buf, stride, P.R, world, P.precision, c->d_result.p, s));
-    CUDA_TRY(c->h_result.reserve(64));
-    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, 32, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c->h_result.reserve((1 + world) * 32));
+    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (1 + world) * 32, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    std::memcpy(&res, c->h_result.p, 32);
+    const uint64_t* h = c->h_result.as<uint64_t>();
+    std::memcpy(&res, h, 32);
+    for (int q = 0; q < world; ++q)
+        if (h[4 * (1 + q) + 1] != 0 && out.failed_rank < 0) {
+            out.failed_rank = q;
+            out.failed_status = (int)h[4 * (1 + q) + 1];
+        }
+}
+
+void run_colsum(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint32_t column, ColResult& res) {
+    Trace trace_run("sstat.column_sum");
+    BinFile file;
+    ColLocal cl;
+    Outcome out;
+    const int world = c->world;
+    if (world == 1) {
+        colsum_local(c, src, P, column, file, cl);
+        colsum_fold(c, P, cl.rank_buf, cl.stride, 1, res, out);
+        return;
+    }
+    Fail local;
+    bool failed = false;
+    try {
+        colsum_local(c, src, P, column, file, cl);
+    } catch (const Fail& f) {
+        local = f;
+        failed = true;
+    }
+    if (failed) {
+        try {
+            colsum_publish(c, P, cl, local.status);
+        } catch (const Fail&) {
+            throw local;
+        }
+    }
+    CUDA_TRY(c->d_gather.reserve(cl.stride * 32 * world));
+    ncclResult_t r = ncclAllGather(cl.rank_buf, c->d_gather.p, cl.stride * 4, ncclDouble, c->comm, c->stream);
+    if (r != ncclSuccess) throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r)};
+    colsum_fold(c, P, c->d_gather.p, cl.stride, world, res, out);
+    if (failed) throw local;
+    if (out.failed_rank >= 0) throw peer_failure(out);
+}
+
+// ---- device groups (one process, G devices) ----
+
+// Runs fn(i) for every member on the group's host threads (one per member), each bound to its
+// member's device and holding its lock.  Returns each member's failure (failed[i] != 0).
+template <class Fn>
+void group_each(sstat_cuda_ctx* g, std::vector<Fail>& fails, std::vector<char>& failed, Fn&& fn) {
+    const size_t G = g->members.size();
+    fails.assign(G, Fail{});
+    failed.assign(G, 0);
+    g->gpool->run(G, [&](size_t i) {
+        sstat_cuda_ctx* m = g->members[i];
+        std::lock_guard<std::mutex> lk(m->mu);
+        cudaSetDevice(m->device);
+        try {
+            fn(i, m);
+        } catch (const Fail& f) {
+            fails[i] = f;
+            failed[i] = 1;
+        } catch (const std::exception& e) {
+            fails[i] = Fail{SSTAT_ERR_INVALID, e.what()};
+            failed[i] = 1;
+        }
+    });
+}
+
+// A member that failed publishes its status in its rank header exactly like a failing rank of
+// a multi-process communicator, and the exchange and fold still run, so the group exercises
+// the same failure path on one GPU.  Members whose device cannot publish end the call here
+// (after every member's queued work drained).  Returns the lowest failed member or -1.
+int group_publish(sstat_cuda_ctx* g, const std::vector<Fail>& fails, const std::vector<char>& failed,
+                  const std::function<void(size_t, sstat_cuda_ctx*, int)>& publish) {
+    int first = -1;
+    bool stuck = false;
+    for (size_t i = 0; i < g->members.size(); ++i) {
+        if (!failed[i]) continue;
+        if (first < 0) first = (int)i;
+        sstat_cuda_ctx* m = g->members[i];
+        std::lock_guard<std::mutex> lk(m->mu);
+        cudaSetDevice(m->device);
+        try {
+            publish(i, m, fails[i].status);
+        } catch (const Fail&) {
+            stuck = true;
+        }
+    }
+    if (stuck) {
+        for (sstat_cuda_ctx* m : g->members) {
+            std::lock_guard<std::mutex> lk(m->mu);
+            cudaSetDevice(m->device);
+            cudaStreamSynchronize(m->stream);
+            cudaStreamSynchronize(m->copy);
+            cudaGetLastError();
+        }
+        throw fails[first];
+    }
+    return first;
+}
+
+// Moves every member's rank buffer (stride_doubles each, at bufs[i]) into member 0's gather
+// buffer in rank order: grouped ncclAllGather over the ncclCommInitAll communicators, or peer
+// copies (cudaMemcpyPeerAsync over NVLink) ordered after each member's stream.  Returns member
+// 0's gathered buffer; member 0's stream is ordered after every contribution.
+void* group_gather(sstat_cuda_ctx* g, const std::vector<const void*>& bufs, uint64_t stride_doubles) {
+    const int G = (int)g->members.size();
+    sstat_cuda_ctx* m0 = g->members[0];
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (sstat_cuda_ctx* m : g->members) locks.emplace_back(m->mu);
+    const uint64_t bytes = stride_doubles * 8;
+    if (g->peer) {
+        CUDA_TRY(cudaSetDevice(m0->device));
+        CUDA_TRY(m0->d_gather.reserve(bytes * G));
+        for (int i = 0; i < G; ++i) {
+            sstat_cuda_ctx* m = g->members[i];
+            if (i > 0) {
+                CUDA_TRY(cudaSetDevice(m->device));
+                CUDA_TRY(cudaEventRecord(m->ev[5], m->stream));
+                CUDA_TRY(cudaSetDevice(m0->device));
+                CUDA_TRY(cudaStreamWaitEvent(m0->stream, m->ev[5], 0));
+            }
+            CUDA_TRY(cudaMemcpyPeerAsync(m0->d_gather.as<char>() + i * bytes, m0->device, bufs[i], m->device, bytes,
+                                         m0->stream));
+        }
+        return m0->d_gather.p;
+    }
+    for (sstat_cuda_ctx* m : g->members) {
+        CUDA_TRY(cudaSetDevice(m->device));
+        CUDA_TRY(m->d_gather.reserve(bytes * G));
+    }
+    ncclResult_t r = ncclGroupStart();
+    for (int i = 0; i < G && r == ncclSuccess; ++i) {
+        sstat_cuda_ctx* m = g->members[i];
+        r = ncclAllGather(bufs[i], m->d_gather.p, stride_doubles, ncclDouble, m->comm, m->stream);
+    }
+    const ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        throw Fail{SSTAT_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r != ncclSuccess ? r : r2)};
+    CUDA_TRY(cudaSetDevice(m0->device));
+    return m0->d_gather.p;
+}
+
+// Sources of a group call: DEVICE = one source per member (its shard, on its device);
+// HOST / FILE = one source every member reads its own ranges from.
+const sstat_cuda_source* member_src(const sstat_cuda_source* src, size_t i) {
+    return src->kind == SSTAT_SRC_DEVICE ? src + i : src;
+}
+
+void sum_timings(sstat_cuda_timings* tm, const std::vector<sstat_cuda_timings>& tms) {
+    if (!tm) return;
+    for (const auto& t : tms) {
+        tm->h2d_seconds = std::max(tm->h2d_seconds, t.h2d_seconds);
+        tm->kernel_seconds = std::max(tm->kernel_seconds, t.kernel_seconds);
+        tm->fold_seconds = std::max(tm->fold_seconds, t.fold_seconds);
+        tm->bytes_read += t.bytes_read;
+        tm->h2d_bytes += t.h2d_bytes;
+        tm->kernel_launches += t.kernel_launches;
+        tm->n_local_ranges += t.n_local_ranges;
+    }
+}
+
+// dataset_suffstats / co-moments over a device group: every member accumulates its contiguous
+// share of the ranges in parallel (rank i of G, the same shard rule as the multi-process path),
+// the rank buffers meet in member 0, and member 0 runs the same fold — bit-identical to one GPU
+// and to G processes.
+void run_group(sstat_cuda_ctx* g, const sstat_cuda_source* src, const Plan& P0, double* result_host, Outcome& out,
+               sstat_cuda_timings* tm) {
+    Trace trace_run(P0.mode == Mode::Comoments ? "sstat.group.comoments" : "sstat.group.dataset");
+    const size_t G = g->members.size();
+    std::vector<Plan> Ps(G, P0);
+    std::vector<Local> sts(G);
+    std::vector<BinFile> files(G);
+    std::vector<sstat_cuda_timings> tms(G);
+    std::vector<Fail> fails;
+    std::vector<char> failed;
+    for (size_t i = 0; i < G; ++i) classify(Ps[i], sts[i]);
+    group_each(g, fails, failed, [&](size_t i, sstat_cuda_ctx* m) {
+        run_local(m, member_src(src, i), Ps[i], files[i], sts[i], tm ? &tms[i] : nullptr);
+    });
+    const int first_failed = group_publish(g, fails, failed, [&](size_t i, sstat_cuda_ctx* m, int status) {
+        publish_status(m, Ps[i], sts[i], status);
+    });
+    std::vector<const void*> bufs(G);
+    for (size_t i = 0; i < G; ++i) bufs[i] = sts[i].rank_buf;
+    const double* fold_buf = static_cast<const double*>(group_gather(g, bufs, sts[0].rank_stride));
+    sstat_cuda_ctx* m0 = g->members[0];
+    std::lock_guard<std::mutex> lk(m0->mu);
+    sstat_cuda_timings t0{};
+    run_fold(m0, member_src(src, 0), Ps[0], sts[0], fold_buf, (int)G, result_host, out, tm ? &t0 : nullptr);
+    if (first_failed >= 0) {
+        if (out.failed_rank != first_failed)
+            throw Fail{SSTAT_ERR_CUDA, "group: rank headers disagree with the members' failures"};
+        throw fails[first_failed];
+    }
+    if (tm) {
+        tms[0].fold_seconds += t0.fold_seconds;
+        tms[0].exchange_seconds += t0.exchange_seconds;
+        tms[0].kernel_launches += t0.kernel_launches;
+        sum_timings(tm, tms);
+        tm->exchange_seconds = t0.exchange_seconds;
+    }
+}
+
+void run_group_colsum(sstat_cuda_ctx* g, const sstat_cuda_source* src, const Plan& P0, uint32_t column,
+                      ColResult& res) {
+    Trace trace_run("sstat.group.column_sum");
+    const size_t G = g->members.size();
+    std::vector<Plan> Ps(G, P0);
+    std::vector<ColLocal> cls(G);
+    std::vector<BinFile> files(G);
+    std::vector<Fail> fails;
+    std::vector<char> failed;
+    group_each(g, fails, failed,
+               [&](size_t i, sstat_cuda_ctx* m) { colsum_local(m, member_src(src, i), Ps[i], column, files[i], cls[i]); });
+    const int first_failed = group_publish(g, fails, failed, [&](size_t i, sstat_cuda_ctx* m, int status) {
+        colsum_publish(m, Ps[i], cls[i], status);
+    });
+    std::vector<const void*> bufs(G);
+    for (size_t i = 0; i < G; ++i) bufs[i] = cls[i].rank_buf;
+    const void* fold_buf = group_gather(g, bufs, cls[0].stride * 4);
+    sstat_cuda_ctx* m0 = g->members[0];
+    std::lock_guard<std::mutex> lk(m0->mu);
+    Outcome out;
+    colsum_fold(m0, Ps[0], fold_buf, cls[0].stride, (int)G, res, out);
+    if (first_failed >= 0) {
+        if (out.failed_rank != first_failed)
+            throw Fail{SSTAT_ERR_CUDA, "group: rank headers disagree with the members' failures"};
+        throw fails[first_failed];
+    }
 }
 
 // double_equals_int128 (reference src/util.cpp:47-52).
@@ -1094,66 +1513,195 @@ const char* sstat_status_string(int status) {
         case SSTAT_ERR_UNSUPPORTED: return "unsupported";
         case SSTAT_ERR_IO: return "I/O error";
         case SSTAT_ERR_FORMAT: return "format error";
+        case SSTAT_ERR_PEER: return "another rank failed";
         default: return "unknown status";
     }
 }
 
+}  // extern "C"
+
+namespace {
+
+void free_device_state(sstat_cuda_ctx* c) {
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy) cudaStreamSynchronize(c->copy);
+    if (c->side) cudaStreamSynchronize(c->side);
+    if (c->comm) ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+    for (DevBuf* b : {&c->d_meta, &c->d_tiles, &c->d_rank, &c->d_gather, &c->d_shift, &c->d_result, &c->d_flags,
+                      &c->d_counts, &c->d_aux, &c->d_claim, &c->d_pieces})
+        b->release();
+    for (HostBuf* b : {&c->h_meta, &c->h_result, &c->h_shift, &c->h_flags, &c->h_counts, &c->h_pieces}) b->release();
+    for (auto& s : c->slots) s.release();
+    for (auto& b : c->bounce) b.release();
+    for (auto e : c->ev_copied) cudaEventDestroy(e);
+    for (auto e : c->ev_free) cudaEventDestroy(e);
+    for (auto e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    for (cudaStream_t s : {c->own, c->copy, c->cap, c->side})
+        if (s) cudaStreamDestroy(s);
+}
+
+// One device's context.  The context's own stream is a blocking stream: work on it is ordered
+// after the legacy default stream, so a device source written by a default-stream producer
+// (e.g. a torch kernel with no explicit stream) is complete before it is read.
+int init_device(sstat_cuda_ctx* c, int device) {
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) return SSTAT_ERR_CUDA;
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamDefault) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return SSTAT_ERR_CUDA;
+    c->stream = c->own;
+    for (auto& e : c->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return SSTAT_ERR_CUDA;
+    return SSTAT_OK;
+}
+
+int device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+template <class Body>
+int guarded(sstat_cuda_error* err, Body&& body) {
+    try {
+        body();
+        return SSTAT_OK;
+    } catch (const Fail& f) {
+        cudaGetLastError();
+        return report(err, f);
+    } catch (const std::bad_alloc&) {
+        return report(err, Fail{SSTAT_ERR_OOM, "host allocation failed"});
+    } catch (const std::exception& e) {
+        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
+    }
+}
+
+Fail nonfinite_failure(const Plan& P, const Outcome& o, bool in_dataset) {
+    Fail f{SSTAT_ERR_NONFINITE, ""};
+    f.row = o.bad_lin / P.p;
+    f.col = (uint32_t)(o.bad_lin % P.p);
+    if (in_dataset) {
+        f.range = range_of_row(P, f.row);
+        f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
+                ", column " + std::to_string(f.col);
+    } else {
+        f.range = 0;
+        f.msg = "non-finite value at row " + std::to_string(f.row) + ", column " + std::to_string(f.col);
+    }
+    return f;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sstat_cuda_init(sstat_cuda_ctx** out, int device) {
     if (!out) return SSTAT_ERR_INVALID;
     *out = nullptr;
-    int n = 0;
-    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
-        cudaGetLastError();
-        return SSTAT_ERR_CUDA;
-    }
+    const int n = device_count();
+    if (n == 0) return SSTAT_ERR_CUDA;
     if (device < 0) cudaGetDevice(&device);
     if (device >= n) return SSTAT_ERR_INVALID;
     auto* c = new sstat_cuda_ctx;
-    c->device = device;
-    if (cudaSetDevice(device) != cudaSuccess) {
+    const int st = init_device(c, device);
+    if (st != SSTAT_OK) {
+        free_device_state(c);
         delete c;
-        return SSTAT_ERR_CUDA;
+        return st;
     }
-    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) {
-        delete c;
-        return SSTAT_ERR_CUDA;
-    }
-    c->stream = c->own;
-    if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) {
-        delete c;
-        return SSTAT_ERR_CUDA;
-    }
-    for (auto& e : c->ev)
-        if (cudaEventCreate(&e) != cudaSuccess) {
-            delete c;
-            return SSTAT_ERR_CUDA;
-        }
     *out = c;
     return SSTAT_OK;
 }
 
+int sstat_cuda_init_devices(sstat_cuda_ctx** out, int n_gpus, const int* devices) {
+    if (!out || n_gpus < 1 || !devices) return SSTAT_ERR_INVALID;
+    *out = nullptr;
+    const int n = device_count();
+    if (n == 0) return SSTAT_ERR_CUDA;
+    bool distinct = true;
+    for (int i = 0; i < n_gpus; ++i) {
+        if (devices[i] < 0 || devices[i] >= n) return SSTAT_ERR_INVALID;
+        for (int j = 0; j < i; ++j) distinct = distinct && devices[j] != devices[i];
+    }
+    auto* g = new sstat_cuda_ctx;
+    g->device = devices[0];
+    int st = SSTAT_OK;
+    for (int i = 0; i < n_gpus && st == SSTAT_OK; ++i) {
+        auto* m = new sstat_cuda_ctx;
+        g->members.push_back(m);
+        st = init_device(m, devices[i]);
+        m->rank = i;
+        m->world = n_gpus;
+        // the members share the host: feeder threads split between them
+        m->host_threads = std::max(1u, default_host_threads() / (unsigned)n_gpus);
+    }
+    const char* force_peer = getenv("SSTAT_PEER_EXCHANGE");
+    g->peer = n_gpus > 1 && (!distinct || (force_peer && atoi(force_peer) != 0));
+    if (st == SSTAT_OK && n_gpus > 1 && !g->peer) {
+        std::vector<ncclComm_t> comms(n_gpus);
+        if (ncclCommInitAll(comms.data(), n_gpus, devices) != ncclSuccess) st = SSTAT_ERR_NCCL;
+        else
+            for (int i = 0; i < n_gpus; ++i) g->members[i]->comm = comms[i];
+    }
+    if (st == SSTAT_OK && g->peer && distinct)  // direct NVLink copies between member 0 and the rest
+        for (int i = 1; i < n_gpus; ++i) {
+            cudaSetDevice(devices[0]);
+            cudaDeviceEnablePeerAccess(devices[i], 0);
+            cudaSetDevice(devices[i]);
+            cudaDeviceEnablePeerAccess(devices[0], 0);
+            cudaGetLastError();  // already enabled / no P2P: cudaMemcpyPeerAsync still works
+        }
+    if (st != SSTAT_OK) {
+        for (auto* m : g->members) {
+            free_device_state(m);
+            delete m;
+        }
+        delete g;
+        return st;
+    }
+    g->gpool.reset(new FillPool((unsigned)n_gpus));
+    cudaSetDevice(devices[0]);
+    *out = g;
+    return SSTAT_OK;
+}
+
+int sstat_cuda_device_count(const sstat_cuda_ctx* c) {
+    if (!c) return 0;
+    return c->is_group() ? (int)c->members.size() : 1;
+}
+
 int sstat_cuda_destroy(sstat_cuda_ctx* c) {
     if (!c) return SSTAT_OK;
+    if (c->is_group()) {
+        {
+            std::lock_guard<std::mutex> lk(c->mu);
+            c->gpool.reset();
+            for (auto* m : c->members) {
+                std::lock_guard<std::mutex> lm(m->mu);
+                free_device_state(m);
+            }
+        }
+        for (auto* m : c->members) delete m;
+        delete c;
+        return SSTAT_OK;
+    }
     {
         Guard g(c);
-        cudaStreamSynchronize(c->stream);
-        cudaStreamSynchronize(c->copy);
-        if (c->comm) ncclCommDestroy(c->comm);
-        for (DevBuf* b : {&c->d_meta, &c->d_tiles, &c->d_rank, &c->d_gather, &c->d_shift, &c->d_result, &c->d_flags,
-                          &c->d_counts, &c->d_aux, &c->d_claim})
-            b->release();
-        for (HostBuf* b : {&c->h_meta, &c->h_result, &c->h_shift, &c->h_flags, &c->h_counts}) b->release();
-        for (auto& s : c->slots) s.release();
-        for (auto& b : c->bounce) b.release();
-        for (auto e : c->ev_copied) cudaEventDestroy(e);
-        for (auto e : c->ev_free) cudaEventDestroy(e);
-        for (auto e : c->ev) cudaEventDestroy(e);
-        if (c->graph) cudaGraphExecDestroy(c->graph);
-        cudaStreamDestroy(c->own);
-        cudaStreamDestroy(c->copy);
-        cudaStreamDestroy(c->cap);
+        free_device_state(c);
     }
     delete c;
     return SSTAT_OK;
@@ -1161,6 +1709,7 @@ int sstat_cuda_destroy(sstat_cuda_ctx* c) {
 
 int sstat_cuda_set_stream(sstat_cuda_ctx* c, void* stream) {
     if (!c) return SSTAT_ERR_INVALID;
+    if (c->is_group()) return stream ? SSTAT_ERR_UNSUPPORTED : SSTAT_OK;  // members keep their own streams
     Guard g(c);
     c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
     return SSTAT_OK;
@@ -1168,6 +1717,11 @@ int sstat_cuda_set_stream(sstat_cuda_ctx* c, void* stream) {
 
 int sstat_cuda_set_staging(sstat_cuda_ctx* c, uint32_t slots, uint64_t slot_bytes) {
     if (!c || slots < 2 || slot_bytes < (1u << 20)) return SSTAT_ERR_INVALID;
+    if (c->is_group()) {
+        for (auto* m : c->members)
+            if (int st = sstat_cuda_set_staging(m, slots, slot_bytes)) return st;
+        return SSTAT_OK;
+    }
     Guard g(c);
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->copy);
@@ -1181,11 +1735,17 @@ int sstat_cuda_set_staging(sstat_cuda_ctx* c, uint32_t slots, uint64_t slot_byte
     c->ev_free.clear();
     c->n_slots = slots;
     c->slot_bytes = slot_bytes & ~(uint64_t)127;
+    c->slot_cap = 0;
     return SSTAT_OK;
 }
 
 int sstat_cuda_set_host_threads(sstat_cuda_ctx* c, uint32_t threads) {
     if (!c || threads > 1024) return SSTAT_ERR_INVALID;
+    if (c->is_group()) {
+        for (auto* m : c->members)
+            if (int st = sstat_cuda_set_host_threads(m, threads)) return st;
+        return SSTAT_OK;
+    }
     Guard g(c);
     c->host_threads = threads;
     c->pool.reset();
@@ -1201,7 +1761,7 @@ int sstat_cuda_nccl_unique_id(void* id_out, size_t id_bytes) {
 }
 
 int sstat_cuda_comm_init(sstat_cuda_ctx* c, int rank, int world, const void* id, size_t id_bytes) {
-    if (!c || world < 1 || rank < 0 || rank >= world) return SSTAT_ERR_INVALID;
+    if (!c || c->is_group() || world < 1 || rank < 0 || rank >= world) return SSTAT_ERR_INVALID;
     Guard g(c);
     if (c->comm) {
         ncclCommDestroy(c->comm);
@@ -1238,9 +1798,9 @@ int sstat_cuda_dataset(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t
         return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
     const double t0 = now_s();
     if (tm) std::memset(tm, 0, sizeof *tm);
-    try {
+    return guarded(err, [&] {
         Guard g(c);
-        if (c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
+        if (!c->is_group() && c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
         Plan P{};
         P.p = p;
         P.precision = precision;
@@ -1250,27 +1810,17 @@ int sstat_cuda_dataset(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t
         P.counts = range_count;
         std::vector<double> result(partial_len(p ? p : 1));
         Outcome o;
-        run(c, src, P, result.data(), o, tm);
-        if (o.bad_lin != kNone) {
-            Fail f{SSTAT_ERR_NONFINITE, ""};
-            f.row = o.bad_lin / p;
-            f.col = (uint32_t)(o.bad_lin % p);
-            f.range = range_of_row(P, f.row);
-            f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
-                    ", column " + std::to_string(f.col);
-            throw f;
-        }
-        *n_out = P.total;
+        if (c->is_group()) run_group(c, src, P, result.data(), o, tm);
+        else run(c, src, P, result.data(), o, tm);
+        if (o.bad_lin != kNone) throw nonfinite_failure(P, o, true);
+        if (o.failed_rank >= 0) throw peer_failure(o);
+        uint64_t total = 0;
+        for (uint64_t i = 0; i < n_ranges; ++i) total += range_count[i];
+        *n_out = total;
         std::memcpy(sums_out, result.data(), p * 8);
         std::memcpy(cross_out, result.data() + p, (partial_len(p) - p) * 8);
         if (tm) tm->total_seconds = now_s() - t0;
-        return SSTAT_OK;
-    } catch (const Fail& f) {
-        cudaGetLastError();
-        return report(err, f);
-    } catch (const std::exception& e) {
-        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
-    }
+    });
 }
 
 int sstat_cuda_accumulate(sstat_cuda_ctx* c, const double* rows, uint64_t n_rows, uint32_t p, uint64_t start_row,
@@ -1280,14 +1830,26 @@ int sstat_cuda_accumulate(sstat_cuda_ctx* c, const double* rows, uint64_t n_rows
     if (!c || !n_out || !sums_out || !cross_out) return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
     if (p == 0) return report(err, Fail{SSTAT_ERR_INVALID, "schema: column count must be >= 1"});
     if (precision > 1) return report(err, Fail{SSTAT_ERR_INVALID, "unknown precision mode"});
-    try {
+    if (c->is_group()) {  // one chunk: the member whose device holds it (host chunks: member 0)
+        cudaPointerAttributes attr{};
+        sstat_cuda_ctx* m = c->members[0];
+        if (rows && cudaPointerGetAttributes(&attr, rows) == cudaSuccess && attr.type == cudaMemoryTypeDevice)
+            for (auto* q : c->members)
+                if (q->device == attr.device) {
+                    m = q;
+                    break;
+                }
+        cudaGetLastError();
+        return sstat_cuda_accumulate(m, rows, n_rows, p, start_row, precision, flags, n_out, sums_out, cross_out, err);
+    }
+    return guarded(err, [&] {
         Guard g(c);
         const uint64_t E = partial_len(p);
         if (n_rows == 0) {
             *n_out = 0;
             std::memset(sums_out, 0, p * 8);
             std::memset(cross_out, 0, (E - p) * 8);
-            return SSTAT_OK;
+            return;
         }
         if (!rows) throw Fail{SSTAT_ERR_INVALID, "null row pointer"};
         cudaPointerAttributes attr{};
@@ -1312,24 +1874,11 @@ int sstat_cuda_accumulate(sstat_cuda_ctx* c, const double* rows, uint64_t n_rows
         std::vector<double> result(E);
         Outcome o;
         run(c, &src, P, result.data(), o, nullptr);
-        if (o.bad_lin != kNone) {
-            Fail f{SSTAT_ERR_NONFINITE, ""};
-            f.row = o.bad_lin / p;
-            f.col = (uint32_t)(o.bad_lin % p);
-            f.range = 0;
-            f.msg = "non-finite value at row " + std::to_string(f.row) + ", column " + std::to_string(f.col);
-            throw f;
-        }
+        if (o.bad_lin != kNone) throw nonfinite_failure(P, o, false);
         *n_out = n_rows;
         std::memcpy(sums_out, result.data(), p * 8);
         std::memcpy(cross_out, result.data() + p, (E - p) * 8);
-        return SSTAT_OK;
-    } catch (const Fail& f) {
-        cudaGetLastError();
-        return report(err, f);
-    } catch (const std::exception& e) {
-        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
-    }
+    });
 }
 
 int sstat_cuda_range_partials(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t p,
@@ -1339,7 +1888,10 @@ int sstat_cuda_range_partials(sstat_cuda_ctx* c, const sstat_cuda_source* src, u
     if (err) std::memset(err, 0, sizeof *err);
     if (!c || !src || (!partials_out && last_range > first_range))
         return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
-    try {
+    if (c->is_group())  // the window on member 0 (its source: the first of a DEVICE source array)
+        return sstat_cuda_range_partials(c->members[0], src, p, range_start, range_count, n_ranges, first_range,
+                                         last_range, precision, flags, partials_out, err);
+    return guarded(err, [&] {
         Guard g(c);
         Plan P{};
         P.mode = Mode::Partials;
@@ -1354,22 +1906,8 @@ int sstat_cuda_range_partials(sstat_cuda_ctx* c, const sstat_cuda_source* src, u
         P.counts = range_count;
         Outcome o;
         run(c, src, P, nullptr, o, nullptr);
-        if (o.bad_lin != kNone) {
-            Fail f{SSTAT_ERR_NONFINITE, ""};
-            f.row = o.bad_lin / p;
-            f.col = (uint32_t)(o.bad_lin % p);
-            f.range = range_of_row(P, f.row);
-            f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
-                    ", column " + std::to_string(f.col);
-            throw f;
-        }
-        return SSTAT_OK;
-    } catch (const Fail& f) {
-        cudaGetLastError();
-        return report(err, f);
-    } catch (const std::exception& e) {
-        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
-    }
+        if (o.bad_lin != kNone) throw nonfinite_failure(P, o, true);
+    });
 }
 
 int sstat_fold_ranges_host(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
@@ -1388,9 +1926,9 @@ int sstat_cuda_column_sum(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint3
                           uint32_t precision, uint32_t flags, sstat_column_sum_result* out, sstat_cuda_error* err) {
     if (err) std::memset(err, 0, sizeof *err);
     if (!c || !src || !out) return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
-    try {
+    return guarded(err, [&] {
         Guard g(c);
-        if (c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
+        if (!c->is_group() && c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
         Plan P{};
         P.p = p;
         P.precision = precision;
@@ -1399,7 +1937,8 @@ int sstat_cuda_column_sum(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint3
         P.starts = range_start;
         P.counts = range_count;
         ColResult r{};
-        run_colsum(c, src, P, column, r);
+        if (c->is_group()) run_group_colsum(c, src, P, column, r);
+        else run_colsum(c, src, P, column, r);
         const __int128 exact = (__int128)(((unsigned __int128)r.hi << 64) | r.lo);
         out->float_sum = r.f;
         out->exact_ok = r.bad_row == kNone;
@@ -1407,13 +1946,7 @@ int sstat_cuda_column_sum(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint3
         out->exact_lo = r.lo;
         out->note_row = r.bad_row;
         out->float_matches_exact = out->exact_ok && double_equals_i128(r.f, exact);
-        return SSTAT_OK;
-    } catch (const Fail& f) {
-        cudaGetLastError();
-        return report(err, f);
-    } catch (const std::exception& e) {
-        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
-    }
+    });
 }
 
 int sstat_cuda_comoments(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32_t p, const uint64_t* range_start,
@@ -1421,9 +1954,9 @@ int sstat_cuda_comoments(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32
                          double* mean_out, double* m2_out, sstat_cuda_error* err) {
     if (err) std::memset(err, 0, sizeof *err);
     if (!c || !src || !n_out || !mean_out || !m2_out) return report(err, Fail{SSTAT_ERR_INVALID, "null argument"});
-    try {
+    return guarded(err, [&] {
         Guard g(c);
-        if (c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
+        if (!c->is_group() && c->world > 1 && !c->comm) throw Fail{SSTAT_ERR_INVALID, "communicator not initialised"};
         Plan P{};
         P.mode = Mode::Comoments;
         P.p = p;
@@ -1434,26 +1967,16 @@ int sstat_cuda_comoments(sstat_cuda_ctx* c, const sstat_cuda_source* src, uint32
         P.counts = range_count;
         std::vector<double> result(partial_len(p ? p : 1));
         Outcome o;
-        run(c, src, P, result.data(), o, nullptr);
-        if (o.bad_lin != kNone) {
-            Fail f{SSTAT_ERR_NONFINITE, ""};
-            f.row = o.bad_lin / p;
-            f.col = (uint32_t)(o.bad_lin % p);
-            f.range = range_of_row(P, f.row);
-            f.msg = "range " + std::to_string(f.range) + " failed: non-finite value at row " + std::to_string(f.row) +
-                    ", column " + std::to_string(f.col);
-            throw f;
-        }
-        *n_out = P.total;
+        if (c->is_group()) run_group(c, src, P, result.data(), o, nullptr);
+        else run(c, src, P, result.data(), o, nullptr);
+        if (o.bad_lin != kNone) throw nonfinite_failure(P, o, true);
+        if (o.failed_rank >= 0) throw peer_failure(o);
+        uint64_t total = 0;
+        for (uint64_t i = 0; i < n_ranges; ++i) total += range_count[i];
+        *n_out = total;
         std::memcpy(mean_out, result.data(), p * 8);
         std::memcpy(m2_out, result.data() + p, (partial_len(p) - p) * 8);
-        return SSTAT_OK;
-    } catch (const Fail& f) {
-        cudaGetLastError();
-        return report(err, f);
-    } catch (const std::exception& e) {
-        return report(err, Fail{SSTAT_ERR_INVALID, e.what()});
-    }
+    });
 }
 
 uint64_t sstat_plan_partitions(uint64_t n_rows, uint64_t chunk_rows, uint64_t* starts, uint64_t* counts) {
@@ -1485,6 +2008,16 @@ int sstat_merge(uint32_t p, uint32_t precision, uint64_t* n_a, double* sums_a, d
 int sstat_cuda_generate(sstat_cuda_ctx* c, double* dst, uint32_t kind, uint64_t seed, double mu, uint32_t n_int,
                         uint64_t first_row, uint64_t n_rows, uint32_t p) {
     if (!c || (!dst && n_rows) || p == 0 || kind > 2) return SSTAT_ERR_INVALID;
+    if (c->is_group()) {  // on the member whose device holds dst
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, dst) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
+            cudaGetLastError();
+            return SSTAT_ERR_INVALID;
+        }
+        for (auto* m : c->members)
+            if (m->device == attr.device) return sstat_cuda_generate(m, dst, kind, seed, mu, n_int, first_row, n_rows, p);
+        return SSTAT_ERR_INVALID;
+    }
     Guard g(c);
     cudaError_t e = launch_generate(dst, kind, seed, mu, n_int, first_row, n_rows, p, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);

@@ -104,7 +104,7 @@ __global__ void k_colsum_range_fold(const ColPart* __restrict__ tiles, const uin
 // rows in order, exactly reduce.cpp:43-62 (binary32: f32 += (float)v, stored widened).
 __global__ void k_colsum_seq(const double* __restrict__ base, uint64_t base_row, uint32_t p, uint32_t column,
                              const uint64_t* __restrict__ range_start, const uint64_t* __restrict__ range_count,
-                             uint32_t n_ranges, uint32_t precision, ColPart* ranges) {
+                             uint32_t n_ranges, uint32_t precision, ColPart* ranges, uint32_t resume_first) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_ranges) return;
     const double* col = base + (range_start[r] - base_row) * p + column;
@@ -112,7 +112,14 @@ __global__ void k_colsum_seq(const double* __restrict__ base, uint64_t base_row,
     float f32 = 0.0f;
     u128 ex = 0;
     unsigned long long bad = ~0ull;
-    bool ok = true;
+    if (resume_first && r == 0) {  // a range streamed in pieces: continue its sequential sums
+        const ColPart prev = ranges[0];
+        f = prev.f;
+        f32 = (float)prev.f;
+        ex = ((u128)prev.hi << 64) | prev.lo;
+        bad = prev.bad_row;
+    }
+    bool ok = bad == ~0ull;
     for (uint64_t i = 0; i < range_count[r]; ++i) {
         const double v = col[i * p];
         if (precision == 1) f32 = __fadd_rn(f32, __double2float_rn(v));
@@ -136,11 +143,14 @@ __global__ void k_colsum_seq(const double* __restrict__ base, uint64_t base_row,
 
 // Final ascending fold over all ranges (merge in reduce.cpp:63-74): float sums add in range
 // order from +0.0 (binary32 through float), exact sums add, the note comes from the first
-// failing range in fold order.  Range r of rank q lives at buf + q*stride + kHdr/4... (ColPart
-// slots after a one-ColPart header).  One thread.
+// failing range in fold order.  Range r of rank q lives at buf + q*stride + 1 + (r - first(q))
+// (ColPart slots after a one-ColPart rank header {0, status, 0, 0}).  out[0] = the result,
+// out[1 + q] = rank q's header.  Thread 0 folds.
 __global__ void k_colsum_final(const ColPart* __restrict__ buf, uint64_t rank_stride, uint64_t n_ranges, int world,
                                uint32_t precision, ColPart* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0) return;
+    for (int q = threadIdx.x; q < world; q += blockDim.x) out[1 + q] = buf[(uint64_t)q * rank_stride];  // rank headers
+    if (threadIdx.x != 0) return;
     double f = 0.0;
     float f32 = 0.0f;
     u128 ex = 0;
@@ -271,11 +281,13 @@ __global__ void __launch_bounds__(256) k_comoment_merge(const double* __restrict
 cudaError_t launch_colsum(const double* base, uint64_t base_row, uint32_t p, uint32_t column,
                           const uint64_t* range_start, const uint64_t* range_count, const uint64_t* tile_prefix,
                           uint32_t n_ranges, uint64_t tile_begin, uint64_t tile_end, bool sequential,
-                          uint32_t precision, void* tile_parts, void* range_parts, int sms, cudaStream_t stream) {
+                          uint32_t precision, void* tile_parts, void* range_parts, int sms, bool resume_first,
+                          cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
     if (sequential) {
         k_colsum_seq<<<(n_ranges + 127) / 128, 128, 0, stream>>>(base, base_row, p, column, range_start, range_count,
-                                                                  n_ranges, precision, (ColPart*)range_parts);
+                                                                  n_ranges, precision, (ColPart*)range_parts,
+                                                                  resume_first ? 1u : 0u);
         return cudaGetLastError();
     }
     const uint64_t tiles = tile_end - tile_begin;

@@ -62,8 +62,9 @@ __global__ void k_final_fold_seq(const double* __restrict__ buf, uint64_t rank_s
                                  uint32_t p, uint32_t precision, double* out) {
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t E = partial_len(p);
-    if (blockIdx.x == 0 && threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
-        out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
+    if (blockIdx.x == 0)  // append the rank headers
+        for (uint32_t h = threadIdx.x; h < (uint32_t)world * kHdr; h += blockDim.x)
+            out[E + h] = buf[(h / kHdr) * rank_stride + h % kHdr];
     if (e >= E) return;
     out[e] = fold_entry(buf, rank_stride, n_ranges, world, p, precision, e);
 }
@@ -74,8 +75,9 @@ __global__ void __launch_bounds__(256) k_final_fold_fast(const double* __restric
     __shared__ double sm[256];
     const uint64_t E = partial_len(p);
     const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
-    if (blockIdx.x == 0 && threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
-        out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
+    if (blockIdx.x == 0)  // append the rank headers
+        for (uint32_t h = threadIdx.x; h < (uint32_t)world * kHdr; h += blockDim.x)
+            out[E + h] = buf[(h / kHdr) * rank_stride + h % kHdr];
     const uint64_t e = blockIdx.x * 32ull + le;
     double s = 0.0;
     if (e < E) {  // fold_lane's order, four loads in flight ahead of the adds
@@ -116,7 +118,7 @@ __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, 
 template <typename Acc>
 __global__ void k_refexact(const double* __restrict__ base, uint64_t base_row, const uint64_t* __restrict__ range_start,
                            const uint64_t* __restrict__ range_count, uint32_t p, uint64_t first_range, double* hdr,
-                           double* out, uint32_t* flags) {
+                           double* out, uint32_t* flags, uint32_t resume_first) {
     const uint64_t E = partial_len(p);
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint32_t r = blockIdx.y;
@@ -126,7 +128,7 @@ __global__ void k_refexact(const double* __restrict__ base, uint64_t base_row, c
     if (!is_sum) unpack_index(p, (uint32_t)(e - p), j, k);
     const double* rows = base + (range_start[r] - base_row) * p;
     const uint64_t n = range_count[r];
-    Acc acc = Acc(0);
+    Acc acc = resume_first && r == 0 ? (Acc)out[e] : Acc(0);  // the range's chain continues
     uint64_t i = 0;
     constexpr int U = 8;
     for (; i + U <= n; i += U) {
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(128) k_refexact_staged(const double* __restric
                                                          const uint64_t* __restrict__ range_start,
                                                          const uint64_t* __restrict__ range_count, uint32_t p,
                                                          uint64_t first_range, double* hdr, double* out,
-                                                         uint32_t* flags, uint32_t ch) {
+                                                         uint32_t* flags, uint32_t ch, uint32_t resume_first) {
     extern __shared__ double stage[];  // [2][ch * p]
     const uint64_t E = partial_len(p);
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(128) k_refexact_staged(const double* __restric
         for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) cp_async8_ca(dst + i, src + i);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    Acc acc = Acc(0);
+    Acc acc = active && resume_first && r == 0 ? (Acc)out[e] : Acc(0);
     if (n_chunks > 0) issue(0);
     for (uint64_t c = 0; c < n_chunks; ++c) {
         if (c + 1 < n_chunks) {
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(128) k_refexact_tma(const double* __restrict__
                                                       const uint64_t* __restrict__ range_start,
                                                       const uint64_t* __restrict__ range_count, uint32_t p,
                                                       uint64_t first_range, double* hdr, double* out, uint32_t* flags,
-                                                      uint32_t ch) {
+                                                      uint32_t ch, uint32_t resume_first) {
     extern __shared__ __align__(128) double stage[];  // [kRefStages][ch * p] | full[kRefStages]
     const uint32_t chunk_elems = ch * p;
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + kRefStages * chunk_elems);
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(128) k_refexact_tma(const double* __restrict__
         for (uint64_t c = 0; c < n_chunks && c < kRefStages; ++c) issue(c);
     }
     __syncthreads();
-    Acc acc = Acc(0);
+    Acc acc = active && resume_first && r == 0 ? (Acc)out[e] : Acc(0);
     for (uint64_t c = 0; c < n_chunks; ++c) {
         const uint32_t parity = (uint32_t)((c / kRefStages) & 1);
         asm volatile(
@@ -414,8 +416,9 @@ cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t 
 cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_t* range_start,
                             const uint64_t* range_count, uint32_t n_ranges, uint32_t p, uint32_t precision,
                             uint64_t first_range, double* hdr, double* out, uint32_t* flags, bool rows_aligned16,
-                            cudaStream_t stream) {
+                            bool resume_first, cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
+    const uint32_t rf = resume_first ? 1u : 0u;
     const uint64_t E = partial_len(p);
     dim3 grid((unsigned)((E + 127) / 128), n_ranges);
     // TMA ring when every range starts 16-byte aligned (the caller checks; chunks hold an even
@@ -428,12 +431,12 @@ cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_
             e = cudaFuncSetAttribute(k_refexact_tma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
             k_refexact_tma<float><<<grid, 128, smem, stream>>>(base, base_row, range_start, range_count, p,
-                                                               first_range, hdr, out, flags, ch);
+                                                               first_range, hdr, out, flags, ch, rf);
         } else {
             e = cudaFuncSetAttribute(k_refexact_tma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
             k_refexact_tma<double><<<grid, 128, smem, stream>>>(base, base_row, range_start, range_count, p,
-                                                                first_range, hdr, out, flags, ch);
+                                                                first_range, hdr, out, flags, ch, rf);
         }
         return cudaGetLastError();
     }
@@ -445,21 +448,21 @@ cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_
             e = cudaFuncSetAttribute(k_refexact_staged<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             if (e != cudaSuccess) return e;
             k_refexact_staged<float><<<grid, 128, smem, stream>>>(base, base_row, range_start, range_count, p,
-                                                                  first_range, hdr, out, flags, ch);
+                                                                  first_range, hdr, out, flags, ch, rf);
         } else {
             e = cudaFuncSetAttribute(k_refexact_staged<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             if (e != cudaSuccess) return e;
             k_refexact_staged<double><<<grid, 128, smem, stream>>>(base, base_row, range_start, range_count, p,
-                                                                   first_range, hdr, out, flags, ch);
+                                                                   first_range, hdr, out, flags, ch, rf);
         }
         return cudaGetLastError();
     }
     if (precision == 1)
         k_refexact<float><<<grid, 128, 0, stream>>>(base, base_row, range_start, range_count, p, first_range, hdr, out,
-                                                    flags);
+                                                    flags, rf);
     else
         k_refexact<double><<<grid, 128, 0, stream>>>(base, base_row, range_start, range_count, p, first_range, hdr, out,
-                                                     flags);
+                                                     flags, rf);
     return cudaGetLastError();
 }
 

@@ -536,7 +536,6 @@ struct Plan {
     WideGeom spare_geo{};
 };
 std::mutex g_plan_mu;
-cudaStream_t g_side[64] = {};  // per-device side stream for the spare plan
 std::vector<Plan> g_plans;
 
 template <int SROWS, int R>
@@ -762,10 +761,6 @@ cudaError_t build_plan(int device, uint32_t p, uint32_t srows, bool wg, Plan& pl
         g2.consumers = pl.geo.consumers;
         e = make_plan_any(device, g2, srows, ps, true, wg);
         if (e != cudaSuccess) return e;
-        if (!g_side[device]) {
-            e = cudaStreamCreateWithFlags(&g_side[device], cudaStreamNonBlocking);
-            if (e != cudaSuccess) return e;
-        }
         pl.has_spare = true;
         pl.spare_ctas = (uint32_t)(slots - used);
         pl.spare_smem = ps.smem;
@@ -779,7 +774,7 @@ cudaError_t build_plan(int device, uint32_t p, uint32_t srows, bool wg, Plan& pl
 uint32_t widep_tile_rows(uint32_t) { return 32768; }
 
 namespace {
-cudaError_t launch_forked(const TileJob& job, const Plan& pl, int device, cudaStream_t stream, uint32_t* kernels);
+cudaError_t launch_forked(const TileJob& job, const Plan& pl, cudaStream_t stream, uint32_t* kernels);
 }
 
 cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t* kernels) {
@@ -842,19 +837,20 @@ cudaError_t launch_widep(const TileJob& job, int, cudaStream_t stream, uint32_t*
             if (!tuned) g_plans.push_back(pl);
         }
     }
-    e = launch_forked(job, pl, device, stream, kernels);
+    e = launch_forked(job, pl, stream, kernels);
     if (tuned) free_plan(pl);  // experiment plans are not cached (cudaFree waits for the launches)
     return e;
 }
 
 namespace {
-cudaError_t launch_forked(const TileJob& job, const Plan& pl, int device, cudaStream_t stream, uint32_t* kernels) {
-    if (!pl.has_spare || !job.claim || job.tile_end - job.tile_begin < 2 || env_u32("SSTAT_WIDEP_SPARE", 1) == 0)
+cudaError_t launch_forked(const TileJob& job, const Plan& pl, cudaStream_t stream, uint32_t* kernels) {
+    if (!pl.has_spare || !job.claim || !job.side || job.tile_end - job.tile_begin < 2 ||
+        env_u32("SSTAT_WIDEP_SPARE", 1) == 0)
         return launch_plan_any(job, pl, stream);
     cudaError_t e;
-    // fork: the clustered plan on `stream` and the cluster-less plan on the side stream claim
-    // tiles / units dynamically from one word (claim_unit); if the side launch cannot run
-    // alongside, the clustered one simply takes every tile.  Join before returning.
+    // fork: the clustered plan on `stream` and the cluster-less plan on the caller's side
+    // stream claim tiles / units dynamically from one word (claim_unit); if the side launch
+    // cannot run alongside, the clustered one simply takes every tile.  Join before returning.
     unsigned long long* W = job.claim;  // the caller's scratch word (one launch at a time per caller)
     if ((e = cudaMemsetAsync(W, 0, sizeof *W, stream)) != cudaSuccess) return e;
     Plan pa = pl, pb = pl;
@@ -865,20 +861,14 @@ cudaError_t launch_forked(const TileJob& job, const Plan& pl, int device, cudaSt
     pb.geo.role = 1;
     pb.grid_cap = pl.spare_ctas;
     pb.smem = pl.spare_smem;
-    cudaStream_t side = g_side[device];
-    cudaEvent_t fork, join;
-    if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) != cudaSuccess) return e;
-    cudaEventRecord(fork, stream);
-    cudaStreamWaitEvent(side, fork, 0);
+    if ((e = cudaEventRecord(job.fork, stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(job.side, job.fork, 0)) != cudaSuccess) return e;
     e = launch_plan_any(job, pa, stream);
-    cudaError_t e2 = launch_plan_any(job, pb, side);
-    cudaEventRecord(join, side);
-    cudaStreamWaitEvent(stream, join, 0);
+    cudaError_t e2 = launch_plan_any(job, pb, job.side);
+    cudaError_t e3 = cudaEventRecord(job.join, job.side);
+    if (e3 == cudaSuccess) e3 = cudaStreamWaitEvent(stream, job.join, 0);
     if (kernels) *kernels = 2;
-    cudaEventDestroy(fork);
-    cudaEventDestroy(join);
-    return e != cudaSuccess ? e : e2;
+    return e != cudaSuccess ? e : e2 != cudaSuccess ? e2 : e3;
 }
 }  // namespace
 

@@ -54,21 +54,25 @@ cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t 
 // Reference-order accumulation: one sequential mul-then-add chain per (range, entry)
 // exactly as accumulate_into<Acc> (suffstats.cpp:56-67); precision 1 = binary32.
 // Writes raw range partials out[r*E] and flags non-finite ranges (flags[r], hdr[0]).
+// resume_first: range 0 of this launch is a later piece of a range streamed in pieces — its
+// chains continue from out[0..E) instead of +0.0 (same operations, same order).
 cudaError_t launch_refexact(const double* base, uint64_t base_row, const uint64_t* range_start,
                             const uint64_t* range_count, uint32_t n_ranges, uint32_t p, uint32_t precision,
                             uint64_t first_range, double* hdr, double* out, uint32_t* flags, bool rows_aligned16,
-                            cudaStream_t stream);
+                            bool resume_first, cudaStream_t stream);
 
 // K5: synthetic rows [first_row, first_row + n_rows) (bit-identical to the oracle).
 cudaError_t launch_generate(double* dst, uint32_t kind, uint64_t seed, double mu, uint32_t n_int, uint64_t first_row,
                             uint64_t n_rows, uint32_t p, cudaStream_t stream);
 
 // ---- column_sum (reduce.cpp:32-88): 32-byte partials {f64/f32 sum, exact lo, exact hi,
-// first non-integral row}; tiles -> ranges -> one ascending final fold ----
+// first non-integral row}; tiles -> ranges -> one ascending final fold.  sequential +
+// resume_first: range 0 continues the partial already in range_parts[0] (pieces) ----
 cudaError_t launch_colsum(const double* base, uint64_t base_row, uint32_t p, uint32_t column,
                           const uint64_t* range_start, const uint64_t* range_count, const uint64_t* tile_prefix,
                           uint32_t n_ranges, uint64_t tile_begin, uint64_t tile_end, bool sequential,
-                          uint32_t precision, void* tile_parts, void* range_parts, int sms, cudaStream_t stream);
+                          uint32_t precision, void* tile_parts, void* range_parts, int sms, bool resume_first,
+                          cudaStream_t stream);
 cudaError_t launch_colsum_range_fold(const void* tile_parts, const uint64_t* tile_prefix, uint32_t n_ranges,
                                      void* range_parts, cudaStream_t stream);
 cudaError_t launch_colsum_final(const void* buf, uint64_t rank_stride_parts, uint64_t n_ranges, int world,

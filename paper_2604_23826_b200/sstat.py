@@ -98,9 +98,42 @@ class RowRange:
     row_count: int = 0
 
 
+class _RangeList(list):
+    """A list of RowRange that counts its own mutations: the key of Partition's cached C-ABI
+    arrays, so any in-place change (item assignment, append, sort, ...) rebuilds them while an
+    unchanged plan costs O(1) per call.  RowRange is frozen, so elements cannot change in place."""
+
+    __slots__ = ("version",)
+
+    def __init__(self, items=()):
+        super().__init__(items)
+        self.version = 0
+
+
+def _counting(name):
+    base = getattr(list, name)
+
+    def method(self, *args, **kwargs):
+        self.version += 1
+        return base(self, *args, **kwargs)
+
+    method.__name__ = name
+    return method
+
+
+for _name in ("__setitem__", "__delitem__", "__iadd__", "__imul__", "append", "extend", "insert", "pop", "remove",
+              "clear", "sort", "reverse"):
+    setattr(_RangeList, _name, _counting(_name))
+
+
 @dataclass
 class Partition:
     ranges: List[RowRange] = field(default_factory=list)
+
+    def __setattr__(self, name, value):
+        if name == "ranges" and not isinstance(value, _RangeList):
+            value = _RangeList(value)
+        object.__setattr__(self, name, value)
 
     def total_rows(self) -> int:
         return sum(r.row_count for r in self.ranges)
@@ -114,7 +147,7 @@ class Partition:
         return self._cached()[3]
 
     def _cached(self):
-        key = (id(self.ranges), len(self.ranges), self.ranges[-1] if self.ranges else None)
+        key = (id(self.ranges), self.ranges.version, len(self.ranges))
         cached = getattr(self, "_arrays", None)
         if cached is None or cached[0] != key:
             starts = np.fromiter((r.start_row for r in self.ranges), dtype=np.uint64, count=len(self.ranges))
@@ -287,8 +320,10 @@ def merge_suffstats(a: SuffStats, b: SuffStats) -> SuffStats:
 
 
 # ---------------------------------------------------------------- the engine
-def _raise(status: int, err: N.Error, in_dataset: bool) -> None:
+def _raise(status: int, err: N.Error, in_dataset: bool, reader=None) -> None:
     msg = err.msg.decode(errors="replace")
+    if status == N.ERR_IO and isinstance(reader, RowReader) and reader.error is not None:
+        raise IoError(f"{msg}: {reader.error!r}") from reader.error
     if status == N.ERR_NONFINITE:
         nf = NonFiniteError(err.row, err.col, f"non-finite value at row {err.row}, column {err.col}")
         if in_dataset:
@@ -311,16 +346,54 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
-class Engine:
-    """One CUDA context of the B200 engine (sstat_cuda_ctx), bound to one device."""
+class RowReader:
+    """A dataset served by a callback: BinaryReader::read_rows (binfile.cpp:140-161) as the C
+    ABI's SSTAT_SRC_READER.  ``read(first_row, n_rows, scratch) -> address`` either fills the
+    pinned ``scratch`` buffer (n_rows * p * 8 bytes at that address) and returns it, or returns
+    the address of host memory already holding the rows (pinned memory goes to the device by
+    DMA directly), valid until the pass returns; 0 / None = read failure.  ``n_rows`` = the
+    dataset's rows.  The engine calls it once per staging slot (256 MiB by default)."""
 
-    def __init__(self, device: Optional[int] = None):
+    def __init__(self, read, n_rows: int, first_row: int = 0):
+        self.n_rows, self.first_row = int(n_rows), int(first_row)
+        self.error: Optional[BaseException] = None
+
+        def trampoline(_user, row, n, scratch):
+            try:
+                return int(read(row, n, scratch) or 0) or None
+            except BaseException as e:  # surfaced as IoError by the engine's NULL path
+                self.error = e
+                return None
+
+        self._fn = N.READ_ROWS_FN(trampoline)  # kept alive with the reader
+
+
+class Engine:
+    """One context of the B200 engine (sstat_cuda_ctx): one device, or with ``devices`` a
+    device group — one process driving several GPUs (sstat_cuda_init_devices)."""
+
+    def __init__(self, device: Optional[int] = None, devices: Optional[Sequence[int]] = None):
         self._lib = N.load()
         self._ctx = ctypes.c_void_p()
-        st = self._lib.sstat_cuda_init(ctypes.byref(self._ctx), -1 if device is None else int(device))
-        if st != N.OK:
-            raise DeviceError(st, f"sstat_cuda_init failed: {N.status_string(st)}")
+        if devices is not None:
+            devs = [int(d) for d in devices]
+            arr = (ctypes.c_int * len(devs))(*devs)
+            st = self._lib.sstat_cuda_init_devices(ctypes.byref(self._ctx), len(devs), arr)
+            if st != N.OK:
+                raise DeviceError(st, f"sstat_cuda_init_devices failed: {N.status_string(st)}")
+            self.devices = devs
+        else:
+            st = self._lib.sstat_cuda_init(ctypes.byref(self._ctx), -1 if device is None else int(device))
+            if st != N.OK:
+                raise DeviceError(st, f"sstat_cuda_init failed: {N.status_string(st)}")
+            self.devices = [device]
         self.rank, self.world = 0, 1
+        self._stream_explicit = False  # set_stream called: never re-bind
+        self._stream_bound = None  # the torch stream handle the context currently launches on
+
+    @property
+    def n_devices(self) -> int:
+        return len(self.devices)
 
     def close(self) -> None:
         if self._ctx:
@@ -335,8 +408,22 @@ class Engine:
 
     # -- configuration
     def set_stream(self, cuda_stream: int) -> None:
-        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream).
+        Without this call, a CUDA-tensor source binds the context to torch's current stream of
+        the tensor's device, so the pass is ordered after whatever produced the tensor."""
         self._check(self._lib.sstat_cuda_set_stream(self._ctx, ctypes.c_void_p(cuda_stream or None)))
+        self._stream_explicit = True
+        self._stream_bound = cuda_stream
+
+    def _follow_torch_stream(self, tensor) -> None:
+        if self._stream_explicit or self.n_devices > 1:
+            return  # group members keep their own (blocking) streams
+        import torch
+
+        h = torch.cuda.current_stream(tensor.device).cuda_stream
+        if h != self._stream_bound:
+            self._check(self._lib.sstat_cuda_set_stream(self._ctx, ctypes.c_void_p(h or None)))
+            self._stream_bound = h
 
     def set_staging(self, slots: int, slot_bytes: int) -> None:
         self._check(self._lib.sstat_cuda_set_staging(self._ctx, slots, slot_bytes))
@@ -391,25 +478,16 @@ class Engine:
                           first_row: int = 0, n_rows: Optional[int] = None) -> SuffStats:
         """dataset_suffstats (suffstats.cpp:279-288).
 
-        dataset: an SSTATBIN path, a CUDA tensor (HBM-resident rows), or a host array
-        (numpy / CPU tensor; pinned memory is copied by DMA).  With a communicator,
-        each rank passes its shard and ``first_row`` = the absolute index of its row 0.
+        dataset: an SSTATBIN path, a CUDA tensor (HBM-resident rows), a host array
+        (numpy / CPU tensor; pinned memory is copied by DMA) or a RowReader.  With a
+        communicator, each rank passes its shard and ``first_row`` = the absolute index of its
+        row 0.  A device group takes a path / host array / reader (every member reads its own
+        ranges) or a list of CUDA tensors, one shard per member in device order (the shard rule
+        of shard_ranges; first rows follow from the plan).
         """
         schema.validate()
         p = schema.column_count()
-        src = N.Source()
-        keep = None
-        if isinstance(dataset, (str, os.PathLike)):
-            src.kind = N.SRC_FILE
-            keep = os.fsencode(os.fspath(dataset))
-            src.path = keep
-        else:
-            ptr, keep = self._rows_pointer(dataset, None)
-            src.kind = N.SRC_DEVICE if _is_torch_cuda(dataset) else N.SRC_HOST
-            src.ptr = ptr
-            rows = n_rows if n_rows is not None else _rows_of(dataset, p)
-            src.first_row = first_row
-            src.n_rows = rows
+        src, keep = self._source(dataset, p, first_row, n_rows, plan)
         a_starts, a_counts, R = plan.partition.addresses()
         # one ctypes buffer [sums | cross] viewed by numpy: no per-call pointer objects
         E = p + p * (p + 1) // 2
@@ -418,12 +496,12 @@ class Engine:
         n = ctypes.c_uint64()
         err = N.Error()
         tm = N.Timings()
-        st = self._lib.sstat_cuda_dataset(self._ctx, ctypes.byref(src), p, a_starts, a_counts, R,
+        st = self._lib.sstat_cuda_dataset(self._ctx, src, p, a_starts, a_counts, R,
                                           int(plan.precision), flags, ctypes.byref(n), a_res, a_res + 8 * p,
                                           ctypes.byref(tm), ctypes.byref(err))
-        del keep
         if st != N.OK:
-            _raise(st, err, in_dataset=True)
+            _raise(st, err, in_dataset=True, reader=dataset)
+        del keep
         flat = np.frombuffer(res, dtype=np.float64)
         out = SuffStats(n.value, flat[:p], flat[p:], schema, PrecisionMode(plan.precision))
         if timings is not None:
@@ -444,12 +522,12 @@ class Engine:
         ranges (run_reduction's partials slots, reduce.hpp:85,108).  Shape (last - first, E)."""
         schema.validate()
         p = schema.column_count()
-        src, keep = self._source(dataset, p, first_row, n_rows)
+        src, keep = self._source(dataset, p, first_row, n_rows, plan)
         starts, counts = plan.partition.arrays()
         E = p + p * (p + 1) // 2
         out = np.zeros((max(last_range - first_range, 0), E))
         err = N.Error()
-        st = self._lib.sstat_cuda_range_partials(self._ctx, ctypes.byref(src), p, starts.ctypes.data,
+        st = self._lib.sstat_cuda_range_partials(self._ctx, src, p, starts.ctypes.data,
                                                  counts.ctypes.data, len(starts), first_range, last_range,
                                                  int(plan.precision), flags,
                                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(err))
@@ -458,19 +536,49 @@ class Engine:
             _raise(st, err, in_dataset=True)
         return out
 
-    def _source(self, dataset, p: int, first_row: int, n_rows: Optional[int]):
+    def _source(self, dataset, p: int, first_row: int, n_rows: Optional[int], plan: Optional[ReductionPlan] = None):
+        """(pointer to sstat_cuda_source[k], objects to keep alive) for a call's dataset."""
+        if isinstance(dataset, (list, tuple)):  # a device group's per-member shards
+            if len(dataset) != self.n_devices or plan is None:
+                raise ValueError(f"expected one CUDA shard per device ({self.n_devices}), got {len(dataset)}")
+            R = len(plan.partition.ranges)
+            srcs = (N.Source * len(dataset))()
+            keep = []
+            for i, shard in enumerate(dataset):
+                if not _is_torch_cuda(shard):
+                    raise TypeError("device-group shards must be CUDA tensors")
+                f, _ = shard_ranges(R, i, len(dataset))
+                _check_width(shard, p)
+                ptr, k = self._rows_pointer(shard, None)
+                keep.append(k)
+                srcs[i].kind = N.SRC_DEVICE
+                srcs[i].ptr = ptr
+                srcs[i].first_row = plan.partition.ranges[f].start_row if f < R else 0
+                srcs[i].n_rows = _rows_of(shard, p)
+            return srcs, (srcs, keep)
         src = N.Source()
         if isinstance(dataset, (str, os.PathLike)):
             keep = os.fsencode(os.fspath(dataset))
             src.kind = N.SRC_FILE
             src.path = keep
+        elif isinstance(dataset, RowReader):
+            keep = dataset
+            dataset.error = None
+            src.kind = N.SRC_READER
+            src.read_rows = dataset._fn
+            src.first_row = dataset.first_row
+            src.n_rows = dataset.n_rows
         else:
+            _check_width(dataset, p)
             ptr, keep = self._rows_pointer(dataset, None)
-            src.kind = N.SRC_DEVICE if _is_torch_cuda(dataset) else N.SRC_HOST
+            cuda = _is_torch_cuda(dataset)
+            if cuda:
+                self._follow_torch_stream(dataset)
+            src.kind = N.SRC_DEVICE if cuda else N.SRC_HOST
             src.ptr = ptr
             src.first_row = first_row
             src.n_rows = n_rows if n_rows is not None else _rows_of(dataset, p)
-        return src, keep
+        return ctypes.pointer(src), (src, keep)
 
     def column_sum(self, dataset, column: int, plan: ReductionPlan, p: Optional[int] = None, flags: int = 0,
                    first_row: int = 0, n_rows: Optional[int] = None) -> ColumnSumResult:
@@ -480,12 +588,14 @@ class Engine:
                 with open(dataset, "rb") as fh:
                     hdr = fh.read(64)
                 p = int.from_bytes(hdr[20:24], "little") if len(hdr) == 64 else 1
+            elif isinstance(dataset, (list, tuple)):
+                p = int(dataset[0].shape[1])
             else:
                 p = int(dataset.shape[1])
-        src, keep = self._source(dataset, p, first_row, n_rows)
+        src, keep = self._source(dataset, p, first_row, n_rows, plan)
         starts, counts = plan.partition.arrays()
         res, err = N.ColumnSum(), N.Error()
-        st = self._lib.sstat_cuda_column_sum(self._ctx, ctypes.byref(src), p, column, starts.ctypes.data,
+        st = self._lib.sstat_cuda_column_sum(self._ctx, src, p, column, starts.ctypes.data,
                                              counts.ctypes.data, len(starts), int(plan.precision), flags,
                                              ctypes.byref(res), ctypes.byref(err))
         del keep
@@ -506,12 +616,12 @@ class Engine:
         """run_reduction(accumulate_comoments, merge_comoments) over the plan (suffstats.cpp:107-159)."""
         schema.validate()
         p = schema.column_count()
-        src, keep = self._source(dataset, p, first_row, n_rows)
+        src, keep = self._source(dataset, p, first_row, n_rows, plan)
         starts, counts = plan.partition.arrays()
         n, err = ctypes.c_uint64(), N.Error()
         mean, m2 = np.zeros(p), np.zeros(p * (p + 1) // 2)
         dp = ctypes.POINTER(ctypes.c_double)
-        st = self._lib.sstat_cuda_comoments(self._ctx, ctypes.byref(src), p, starts.ctypes.data, counts.ctypes.data,
+        st = self._lib.sstat_cuda_comoments(self._ctx, src, p, starts.ctypes.data, counts.ctypes.data,
                                             len(starts), flags, ctypes.byref(n), mean.ctypes.data_as(dp),
                                             m2.ctypes.data_as(dp), ctypes.byref(err))
         del keep
@@ -543,6 +653,20 @@ class Engine:
         if expect is not None and arr.size != expect:
             raise ValueError("chunk values size does not match row_count * column_count")
         return ctypes.c_void_p(arr.ctypes.data if arr.size else None), arr
+
+
+def _check_width(dataset, p: int) -> None:
+    """The rows' width against the schema (check_chunk's width test, suffstats.cpp:33-36):
+    2-D inputs must have p columns, flat inputs a multiple of p values."""
+    shape = tuple(dataset.shape) if hasattr(dataset, "shape") else np.shape(dataset)
+    if len(shape) >= 2:
+        bad, cols = shape[-1] != p, shape[-1]
+    else:
+        numel = int(np.prod(shape)) if shape else 0
+        bad, cols = numel % p != 0, numel
+    if bad:
+        msg = f"range 0 failed: chunk has {cols} columns, schema has {p}"
+        raise ReductionError(0, msg, SchemaMismatchError(f"chunk has {cols} columns, schema has {p}"))
 
 
 def _rows_of(dataset, p: int) -> int:

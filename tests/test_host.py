@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert re.search(rf"\bT {name}\b", nm), name
         assert getattr(lib, name) is not None
-    assert lib.sstat_cuda_abi_version() == 1
+    assert lib.sstat_cuda_abi_version() == 2
 
 
 def test_library_is_sm100a():
