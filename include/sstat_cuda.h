@@ -111,6 +111,7 @@ typedef struct {
     uint64_t h2d_bytes;      /* bytes copied host->device                           */
     uint32_t kernel_launches;/* kernels launched by the call                        */
     uint32_t n_local_ranges; /* ranges this rank accumulated                        */
+    char kernel[96];         /* the accumulate kernel that ran, e.g. "k_smallp<2, true>" */
 } sstat_cuda_timings;
 
 typedef enum {

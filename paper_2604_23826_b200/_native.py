@@ -90,6 +90,7 @@ class Timings(Structure):
         ("h2d_bytes", c_uint64),
         ("kernel_launches", c_uint32),
         ("n_local_ranges", c_uint32),
+        ("kernel", c_char * 96),
     ]
 
 

@@ -40,6 +40,7 @@ struct TileJob {
     // (nullptr: no side launch, the clustered launch takes every tile)
     cudaStream_t side;
     cudaEvent_t fork, join;
+    const void** launched;         // (optional) receives the accumulate kernel the launcher chose
 };
 
 // Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).

@@ -12,6 +12,8 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <cxxabi.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -224,6 +226,7 @@ struct sstat_cuda_ctx {
     cudaStream_t cap = nullptr;  // private capture stream (the caller's stream is never captured)
     cudaGraphExec_t graph = nullptr;
     std::vector<uint64_t> graph_key;
+    const void* last_kernel = nullptr;  // the accumulate kernel the last pass launched (timings)
     // ---- device group (sstat_cuda_init_devices): one process driving G devices ----
     // members[g] is a full per-device context with rank g of world G; the group context itself
     // owns no device state.  Exchange: NCCL (ncclCommInitAll over distinct devices) or peer
@@ -760,6 +763,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
         j.tile_begin = t0;
         j.tile_end = t1;
         j.tile_partials = c->d_tiles.as<double>();
+        j.launched = &c->last_kernel;
         if (wide) {
             CUDA_TRY(c->d_claim.reserve(sizeof(unsigned long long)));
             j.claim = c->d_claim.as<unsigned long long>();
@@ -814,6 +818,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                 j.tile_begin = 0;
                 j.tile_end = nt;
                 j.tile_partials = c->d_tiles.as<double>();
+                j.launched = &c->last_kernel;
                 CUDA_TRY(launch_smallp(j, c->sms, cs));
                 CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
                 CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
@@ -1012,6 +1017,35 @@ const double* exchange(sstat_cuda_ctx* c, const Local& st, int world) {
     return c->d_gather.as<double>();
 }
 
+// "k_smallp<2, true>" for a kernel's host stub (cudaFuncGetName + demangle, namespaces and the
+// parameter list dropped): which accumulate kernel a pass actually ran, for the timings.
+void kernel_name(const void* fn, char* out, size_t cap) {
+    out[0] = 0;
+    if (!fn) return;
+    const char* mangled = nullptr;
+    if (cudaFuncGetName(&mangled, fn) != cudaSuccess || !mangled) {
+        cudaGetLastError();
+        return;
+    }
+    int status = 0;
+    char* dem = abi::__cxa_demangle(mangled, nullptr, nullptr, &status);
+    std::string name = status == 0 && dem ? dem : mangled;
+    std::free(dem);
+    // drop the parameter list (the last top-level '('), then the namespace qualifiers before the
+    // kernel's own name (the last top-level "::")
+    int depth = 0;
+    size_t cut = name.size(), start = 0;
+    for (size_t i = 0; i < name.size(); ++i) {
+        const char ch = name[i];
+        if (ch == '<') ++depth;
+        else if (ch == '>') --depth;
+        else if (ch == '(' && depth == 0 && name.compare(i, 12, "(anonymous n") != 0) cut = i;
+        else if (ch == ':' && depth == 0 && i + 1 < name.size() && name[i + 1] == ':') start = i + 2;
+    }
+    if (cut < start) cut = name.size();
+    std::snprintf(out, cap, "%s", name.substr(start, cut - start).c_str());
+}
+
 // Phase 2: the ascending range fold (K3b) or the co-moment merge over the gathered rank
 // buffers, one read-back of the result and every rank header, then the headers: lowest failing
 // range / first non-finite index over all ranks, and the first rank that reported a failure.
@@ -1071,6 +1105,7 @@ void run_fold(sstat_cuda_ctx* c, const sstat_cuda_source* src, const Plan& P, co
     }
     c->flags_clean = !any_flag;
     if (result_host) std::memcpy(result_host, hres, E * 8);
+    if (tm) kernel_name(c->last_kernel, tm->kernel, sizeof tm->kernel);
     if (tm && st.graphable) {  // the graph records three events: K1, then both folds together
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
@@ -1175,6 +1210,7 @@ void colsum_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, uint
     CUDA_TRY(c->d_rank.reserve(cl.stride * 32));
     CUDA_TRY(c->d_aux.reserve(std::max<uint64_t>(nt, 1) * 32));
     cl.rank_buf = static_cast<char*>(c->d_rank.p);
+    c->flags_clean = false;  // d_rank is shared with the sufficient-statistics header: reset it next time
     CUDA_TRY(cudaMemsetAsync(cl.rank_buf, 0, 32, s));  // header part: status 0
     void* range_parts = cl.rank_buf + 32;
     if (L > 0 && src->kind == SSTAT_SRC_DEVICE) {
@@ -1227,6 +1263,7 @@ void colsum_publish(sstat_cuda_ctx* c, const Plan& P, ColLocal& cl, int status) 
     cl.stride = 1 + (P.R + c->world - 1) / c->world;
     CUDA_TRY(c->d_rank.reserve(cl.stride * 32));
     cl.rank_buf = static_cast<char*>(c->d_rank.p);
+    c->flags_clean = false;
     const uint64_t hdr[4] = {0, (uint64_t)status, 0, 0};
     CUDA_TRY(cudaMemcpyAsync(cl.rank_buf, hdr, sizeof hdr, cudaMemcpyHostToDevice, c->stream));
 }
@@ -1348,6 +1385,7 @@ int group_publish(sstat_cuda_ctx* g, const std::vector<Fail>& fails, const std::
 void* group_gather(sstat_cuda_ctx* g, const std::vector<const void*>& bufs, uint64_t stride_doubles) {
     const int G = (int)g->members.size();
     sstat_cuda_ctx* m0 = g->members[0];
+    if (G == 1) return const_cast<void*>(bufs[0]);  // one member: its own rank buffer
     std::vector<std::unique_lock<std::mutex>> locks;
     for (sstat_cuda_ctx* m : g->members) locks.emplace_back(m->mu);
     const uint64_t bytes = stride_doubles * 8;
@@ -1441,6 +1479,7 @@ void run_group(sstat_cuda_ctx* g, const sstat_cuda_source* src, const Plan& P0, 
         tms[0].kernel_launches += t0.kernel_launches;
         sum_timings(tm, tms);
         tm->exchange_seconds = t0.exchange_seconds;
+        std::memcpy(tm->kernel, t0.kernel, sizeof tm->kernel);
     }
 }
 

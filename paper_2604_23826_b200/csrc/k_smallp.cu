@@ -299,6 +299,7 @@ cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
     k_smallp_x1<NB><<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    if (job.launched) *job.launched = (const void*)k_smallp_x1<NB>;
     return cudaGetLastError();
 }
 
@@ -336,6 +337,7 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
     kern<<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    if (job.launched) *job.launched = (const void*)kern;
     return cudaGetLastError();
 }
 

@@ -263,6 +263,7 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
     k_splitp<NB, W, X1, U><<<(unsigned)grid, kThreads, smem, stream>>>(job, widep_tile_rows(job.p));
+    if (job.launched) *job.launched = (const void*)k_splitp<NB, W, X1, U>;
     return cudaGetLastError();
 }
 

@@ -669,6 +669,8 @@ cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream)
     cudaError_t e = cudaLaunchKernelEx(&cfg, pl.wg ? k_widep_wg<SROWS, R> : k_widep<SROWS, R>, job, pl.geo,
                                        widep_tile_rows(pl.geo.p));
     if (e != cudaSuccess) return e;
+    if (job.launched && pl.geo.role == 0)  // the clustered launch (the spare one is its helper)
+        *job.launched = pl.wg ? (const void*)k_widep_wg<SROWS, R> : (const void*)k_widep<SROWS, R>;
     return cudaGetLastError();
 }
 
