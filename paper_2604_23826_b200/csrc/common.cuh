@@ -8,11 +8,15 @@ namespace sstat_b200 {
 
 // Rows per accumulation tile.  A tile is the deterministic unit of work: its
 // partial depends only on the rows of the tile, so results are bit-identical for
-// any grid size, GPU count or staging layout.  4096 rows x 8 warps x 128 k-steps.
+// any grid size, GPU count or staging layout.  K1's tiles are kTileRows = 4096 rows
+// (8 warps x 128 k-steps) except for plans too small to fill the GPU with them:
+// smallp_tile_rows (engine.cu) then halves the height, down to kMinTileRows, until the
+// whole plan has kFillTiles tiles — a function of the plan alone, the same on every rank.
 constexpr uint32_t kTileRows = 4096;
+constexpr uint32_t kMinTileRows = 256;
+constexpr uint64_t kFillTiles = 2ull * 148 * 4;  // twice K1's resident CTA slots on a B200
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kTileKsteps = kTileRows / 4 / kWarps;  // k-steps per warp per tile
 
 // Number of doubles in one canonical partial: sums[p] then the packed upper triangle.
 __host__ __device__ inline uint64_t partial_len(uint32_t p) { return p + (uint64_t)p * (p + 1) / 2; }
@@ -41,6 +45,7 @@ struct TileJob {
     cudaStream_t side;
     cudaEvent_t fork, join;
     const void** launched;         // (optional) receives the accumulate kernel the launcher chose
+    uint32_t tile_rows;            // K1: rows per tile of this plan (smallp_tile_rows)
 };
 
 // Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).

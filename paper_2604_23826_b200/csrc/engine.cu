@@ -435,7 +435,22 @@ struct Plan {
     std::vector<uint64_t> tile_row, tile_rows;  // host view of local tiles (streaming)
 };
 
-uint64_t tile_rows_for(uint32_t p) { return p > 64 ? widep_tile_rows(p) : kTileRows; }
+// K1's tile height for a plan: kTileRows, or — when the whole plan (every rank's ranges) has
+// fewer than kFillTiles such tiles, so the grid would leave CTA slots idle (C1: 245 tiles for
+// 592 slots) — the largest power of two >= kMinTileRows giving at least kFillTiles tiles.
+// A function of the global plan alone: every rank and GPU count cuts the same tiles.
+uint64_t smallp_tile_rows(const Plan& P) {
+    if (P.total / kTileRows >= kFillTiles) return kTileRows;  // sum of ceil(count / TR) >= total / TR
+    uint64_t TR = kTileRows;
+    for (; TR > kMinTileRows; TR /= 2) {
+        uint64_t tiles = 0;
+        for (uint64_t i = 0; i < P.R && tiles < kFillTiles; ++i) tiles += (P.counts[i] + TR - 1) / TR;
+        if (tiles >= kFillTiles) break;
+    }
+    return TR;
+}
+
+uint64_t tile_rows_for(const Plan& P) { return P.p > 64 ? widep_tile_rows(P.p) : smallp_tile_rows(P); }
 
 struct Outcome {
     uint64_t bad_lin = kNone;  // lowest first-non-finite linear index over all ranks
@@ -713,7 +728,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
     cudaStream_t s = c->stream;
 
     // ---- local plan → device ----
-    const uint64_t TR = tile_rows_for(p);
+    const uint64_t TR = tile_rows_for(P);
     auto tiles_of = [TR](uint64_t count) { return (count + TR - 1) / TR; };
     uint64_t* d_starts = upload_meta(c, P, TR, s);
     uint64_t* d_counts = d_starts + L;
@@ -764,6 +779,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
         j.tile_end = t1;
         j.tile_partials = c->d_tiles.as<double>();
         j.launched = &c->last_kernel;
+        j.tile_rows = (uint32_t)TR;
         if (wide) {
             CUDA_TRY(c->d_claim.reserve(sizeof(unsigned long long)));
             j.claim = c->d_claim.as<unsigned long long>();
@@ -789,8 +805,11 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
         CUDA_TRY(c->h_result.reserve(E * 8 + kHdr * 8));
         CUDA_TRY(c->d_result.reserve((E + kHdr) * 8));  // K3b appends the rank header
         const double* base = static_cast<const double*>(src->ptr);
+        // timed = the graph records the K1 / fold events (each external event node costs ~5 us of
+        // replay, so calls without timings replay a graph without them)
+        const bool timed = tm != nullptr;
         const std::vector<uint64_t> key = {
-            (uint64_t)(uintptr_t)base, src->first_row, p, L, nt, E, P.r0, shift, (uint64_t)(uintptr_t)s,
+            (uint64_t)(uintptr_t)base, src->first_row, p, L, nt, E, P.r0, shift, (uint64_t)(uintptr_t)s, timed, TR,
             c->d_meta.gen, c->d_tiles.gen, c->d_rank.gen, c->d_flags.gen, c->d_shift.gen, c->d_result.gen,
             (uint64_t)(uintptr_t)c->h_result.p, (uint64_t)(uintptr_t)c->d_meta.p, (uint64_t)(uintptr_t)c->d_tiles.p,
             (uint64_t)(uintptr_t)c->d_rank.p, (uint64_t)(uintptr_t)c->d_shift.p, (uint64_t)(uintptr_t)c->d_result.p};
@@ -805,7 +824,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                 if (shift)
                     CUDA_TRY(launch_gather_shift(base, src->first_row, d_starts, d_counts, (uint32_t)L, p,
                                                  c->d_shift.as<double>(), cs));
-                CUDA_TRY(cudaEventRecordWithFlags(c->ev[0], cs, cudaEventRecordExternal));
+                if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[0], cs, cudaEventRecordExternal));
                 TileJob j{};
                 j.base = base;
                 j.base_row = src->first_row;
@@ -819,13 +838,14 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                 j.tile_end = nt;
                 j.tile_partials = c->d_tiles.as<double>();
                 j.launched = &c->last_kernel;
+                j.tile_rows = (uint32_t)TR;
                 CUDA_TRY(launch_smallp(j, c->sms, cs));
-                CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
+                if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
                 CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
                                            (uint32_t)L, p, P.r0, rank_buf, d_flags, cs));
 
                 CUDA_TRY(launch_final_fold(rank_buf, rank_stride, P.R, 1, p, 0u, false, c->d_result.as<double>(), cs));
-                CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
+                if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
                 CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + kHdr) * 8, cudaMemcpyDeviceToHost, cs));
             } catch (...) {
                 cudaStreamEndCapture(c->cap, &g);
@@ -1035,14 +1055,20 @@ void kernel_name(const void* fn, char* out, size_t cap) {
     // kernel's own name (the last top-level "::")
     int depth = 0;
     size_t cut = name.size(), start = 0;
-    for (size_t i = 0; i < name.size(); ++i) {
+    for (size_t i = 0; i < name.size(); ++i) {  // the parameter list: the last top-level '('
         const char ch = name[i];
         if (ch == '<') ++depth;
         else if (ch == '>') --depth;
         else if (ch == '(' && depth == 0 && name.compare(i, 12, "(anonymous n") != 0) cut = i;
-        else if (ch == ':' && depth == 0 && i + 1 < name.size() && name[i + 1] == ':') start = i + 2;
     }
-    if (cut < start) cut = name.size();
+    depth = 0;
+    for (size_t i = 0; i < cut; ++i) {  // the kernel's own name: after the last top-level "::" or ' '
+        const char ch = name[i];
+        if (ch == '<') ++depth;
+        else if (ch == '>') --depth;
+        else if (depth == 0 && ch == ':' && i + 1 < cut && name[i + 1] == ':') start = i + 2;
+        else if (depth == 0 && ch == ' ' && name.compare(i, 10, " namespace") != 0) start = i + 1;
+    }
     std::snprintf(out, cap, "%s", name.substr(start, cut - start).c_str());
 }
 

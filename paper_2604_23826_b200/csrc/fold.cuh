@@ -9,10 +9,12 @@ namespace sstat_b200 {
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
 // Tile folds of one range run kTileLanes interleaved lanes per entry: lane q sums tiles
-// t0+q, t0+q+kTileLanes, ... (up to 8 loads in flight, masked tails instead of a serial
+// t0+q, t0+q+kTileLanes, ... (kFoldInFlight loads in flight, masked tails instead of a serial
 // remainder loop), then the lanes are added 0..kTileLanes-1.  A fixed function of the range's
-// tile partials; blocks are kTileLanes x 32 threads.
-constexpr int kTileLanes = 16;
+// tile partials; blocks are kTileLanes x 32 threads.  32 lanes x 16 loads in flight keep a
+// range of ~2000 small-plan tiles (C1: 1e6 rows in 512-row tiles) to four L2 round trips.
+constexpr int kTileLanes = 32;
+constexpr int kFoldInFlight = 16;
 __device__ __forceinline__ double fold_tiles_lane(const double* __restrict__ tp, uint64_t E, uint64_t e, uint64_t t0,
                                                   uint64_t t1, int q) {
     double s = 0.0;
@@ -21,13 +23,13 @@ __device__ __forceinline__ double fold_tiles_lane(const double* __restrict__ tp,
     const uint32_t cnt = (uint32_t)((T - q + kTileLanes - 1) / kTileLanes);  // this lane's tiles
     const uint64_t stride = (uint64_t)kTileLanes * E;
     const double* ptr = tp + (t0 + q) * E + e;
-    for (uint32_t i = 0; i < cnt; i += 8, ptr += 8 * stride) {
+    for (uint32_t i = 0; i < cnt; i += kFoldInFlight, ptr += kFoldInFlight * stride) {
         const uint32_t m = cnt - i;
-        double v[8];
+        double v[kFoldInFlight];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (uint32_t)u < m ? ld_cg(ptr + u * stride) : 0.0;
+        for (int u = 0; u < kFoldInFlight; ++u) v[u] = (uint32_t)u < m ? ld_cg(ptr + u * stride) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kFoldInFlight; ++u)
             if ((uint32_t)u < m) s += v[u];
     }
     return s;

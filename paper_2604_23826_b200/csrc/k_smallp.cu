@@ -1,7 +1,7 @@
 // k_smallp.cu — K1: streaming sufficient statistics for p <= 64 on the FP64 DMMA pipe.
 //
 // Replaces accumulate_into<double> (reference src/suffstats.cpp:50-70) for one
-// accumulation tile of kTileRows rows.  Each warp walks k-steps of 4 rows.  Lane
+// accumulation tile of job.tile_rows rows (4096; fewer for small plans).  Each warp walks k-steps of 4 rows.  Lane
 // l = 4g + k loads the values of row k at the NB columns col(J, g), J < NB, straight
 // from HBM with coalesced streaming loads (a warp load covers 4 whole rows), subtracts
 // the range shift c, and feeds the same register as the A fragment (A[g][k]) of
@@ -146,9 +146,10 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
     for (uint64_t t = job.tile_begin + blockIdx.x; t < job.tile_end; t += gridDim.x) {
         const uint32_t r = range_of_tile(job.tile_prefix, job.n_ranges, t);
         const uint64_t rs = __ldg(job.range_start + r), rc = __ldg(job.range_count + r);
-        const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + r)) * kTileRows;
+        const uint32_t TR = job.tile_rows;
+        const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + r)) * TR;
         const uint64_t left = rs + rc - row0;
-        const uint32_t rows = left < kTileRows ? (uint32_t)left : kTileRows;
+        const uint32_t rows = left < TR ? (uint32_t)left : TR;
         const double* __restrict__ tile = job.base + (row0 - job.base_row) * p;
 
         // shift row c of this range (the gathered table; reading it in place from the shard

@@ -390,6 +390,10 @@ class Engine:
         self.rank, self.world = 0, 1
         self._stream_explicit = False  # set_stream called: never re-bind
         self._stream_bound = None  # the torch stream handle the context currently launches on
+        # dataset_suffstats fills last_timings (device events around the kernels) unless this is
+        # False and no ReductionTimings is passed: the untimed call skips the event records
+        self.collect_timings = True
+        self.last_timings = None
 
     @property
     def n_devices(self) -> int:
@@ -495,16 +499,16 @@ class Engine:
         a_res = ctypes.addressof(res)
         n = ctypes.c_uint64()
         err = N.Error()
-        tm = N.Timings()
+        tm = N.Timings() if (timings is not None or self.collect_timings) else None
         st = self._lib.sstat_cuda_dataset(self._ctx, src, p, a_starts, a_counts, R,
                                           int(plan.precision), flags, ctypes.byref(n), a_res, a_res + 8 * p,
-                                          ctypes.byref(tm), ctypes.byref(err))
+                                          ctypes.byref(tm) if tm is not None else None, ctypes.byref(err))
         if st != N.OK:
             _raise(st, err, in_dataset=True, reader=dataset)
         del keep
         flat = np.frombuffer(res, dtype=np.float64)
         out = SuffStats(n.value, flat[:p], flat[p:], schema, PrecisionMode(plan.precision))
-        if timings is not None:
+        if timings is not None and tm is not None:
             timings.read_seconds = tm.h2d_seconds
             timings.work_seconds = tm.kernel_seconds + tm.fold_seconds
             timings.bytes_read = tm.bytes_read
