@@ -35,6 +35,7 @@
 
 #include "../../include/sstat_cuda.h"
 #include "common.cuh"
+#include "fold.cuh"
 #include "kernels.h"
 
 using namespace sstat_b200;
@@ -734,6 +735,8 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
     uint64_t* d_counts = d_starts + L;
     uint64_t* d_prefix = d_starts + 2 * L;
     const uint64_t nt = P.n_tiles;
+    uint32_t fold_k = 1;  // K3a's cluster size: the most chunks any local range folds in
+    for (uint64_t i = 0; i < L; ++i) fold_k = std::max(fold_k, fold_chunks(tiles_of(P.counts[P.r0 + i])));
 
     const uint64_t rank_stride = kHdr + P.lmax * E;
     CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
@@ -842,7 +845,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                 CUDA_TRY(launch_smallp(j, c->sms, cs));
                 if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
                 CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
-                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, cs));
+                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, fold_k, cs));
 
                 CUDA_TRY(launch_final_fold(rank_buf, rank_stride, P.R, 1, p, 0u, false, c->d_result.as<double>(), cs));
                 if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
@@ -892,7 +895,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                                                rank_buf + kHdr, P.r0, rank_buf, d_flags, s));
             else
                 CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
-                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
+                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, fold_k, s));
             if (tm) tm->kernel_launches += 2;
         }
         if (world > 1 || P.mode == Mode::Partials) {
@@ -963,7 +966,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                                                rank_buf + kHdr, P.r0, rank_buf, d_flags, s));
             else
                 CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
-                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, s));
+                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, fold_k, s));
             if (tm) tm->kernel_launches += 1;
         }
         // Non-finite localisation: re-stream only the flagged ranges (error path).

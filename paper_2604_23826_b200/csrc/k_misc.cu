@@ -22,23 +22,25 @@ __global__ void k_gather_shift(const double* __restrict__ base, uint64_t base_ro
     shift[i] = range_count[r] ? base[(range_start[r] - base_row) * p + j] : 0.0;
 }
 
-// K3a: blocks of kTileLanes x 32 threads over (local range, cross-entry slice) (fold_range_block).
+// K3a: blocks of kTileLanes x 32 threads over (local range x chunk, cross-entry slice)
+// (fold_range_block); CLUSTER: the K chunk CTAs of a range form one thread-block cluster.
 // The shift row comes from the table, or (shift == nullptr, base != nullptr) in place as the
 // range's first row of the resident shard.
+template <bool CLUSTER>
 __global__ void __launch_bounds__(kTileLanes * 32) k_range_fold(const double* __restrict__ tp,
                                                     const uint64_t* __restrict__ tile_prefix,
                                                     const uint64_t* __restrict__ range_count,
                                                     const double* __restrict__ shift, const double* base,
                                                     uint64_t base_row, const uint64_t* __restrict__ range_start,
                                                     uint32_t p, uint64_t first_range, double* rank_buf,
-                                                    uint32_t* flags, uint64_t slice) {
+                                                    uint32_t* flags, uint64_t slice, uint32_t K) {
     extern __shared__ double sm[];
-    const uint32_t r = blockIdx.x;
+    const uint32_t r = blockIdx.x / K, k = blockIdx.x % K;
     const double* c = shift ? shift + (uint64_t)r * p
                             : (base && range_count[r] ? base + (range_start[r] - base_row) * p : nullptr);
     const uint64_t x0 = (uint64_t)blockIdx.y * slice, x1 = x0 + slice;  // this block's cross entries
-    fold_range_block(tp, tile_prefix[r], tile_prefix[r + 1], (double)range_count[r], c, p, first_range + r,
-                     rank_buf + kHdr + (uint64_t)r * partial_len(p), rank_buf, flags + r, sm, x0, x1);
+    fold_range_block<CLUSTER>(tp, tile_prefix[r], tile_prefix[r + 1], (double)range_count[r], c, p, first_range + r,
+                              rank_buf + kHdr + (uint64_t)r * partial_len(p), rank_buf, flags + r, sm, x0, x1, k);
 }
 
 // Scans the flagged local ranges for their first non-finite value.  Ranges ascend, so
@@ -377,20 +379,35 @@ cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uin
 cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_prefix, const uint64_t* range_count,
                               const double* shift, const double* base, uint64_t base_row, const uint64_t* range_start,
                               uint32_t n_ranges, uint32_t p, uint64_t first_range, double* rank_buf, uint32_t* flags,
-                              cudaStream_t stream) {
+                              uint32_t chunks, cudaStream_t stream) {
     if (n_ranges == 0) return cudaSuccess;
-    const size_t smem = (2 * p + kTileLanes * 32) * sizeof(double);  // fold_range_block scratch
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_range_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    // blocks = ranges x slices of the cross entries; a slice is as wide as the sums so the
-    // redundant sums fold costs at most as much as the slice itself
+    // blocks = ranges x chunks x slices of the cross entries; a slice is as wide as the sums so
+    // the redundant sums fold costs at most as much as the slice itself
     const uint64_t cross = (uint64_t)p * (p + 1) / 2;
     const uint64_t slice = 32ull * ((p + 31) / 32);
-    const dim3 grid(n_ranges, (unsigned)((cross + slice - 1) / slice));
-    k_range_fold<<<grid, kTileLanes * 32, smem, stream>>>(tile_partials, tile_prefix, range_count, shift, base, base_row,
-                                              range_start, p, first_range, rank_buf, flags, slice);
+    const size_t smem = fold_smem_doubles(p, slice) * sizeof(double);
+    const uint32_t K = chunks < 1 ? 1 : chunks;
+    const dim3 grid(n_ranges * K, (unsigned)((cross + slice - 1) / slice));
+    auto kern = K > 1 ? k_range_fold<true> : k_range_fold<false>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kTileLanes * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = K > 1 ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tile_partials, tile_prefix, range_count, shift, base, base_row,
+                                       range_start, p, first_range, rank_buf, flags, slice, K);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

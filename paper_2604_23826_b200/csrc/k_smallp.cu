@@ -1,7 +1,7 @@
 // k_smallp.cu — K1: streaming sufficient statistics for p <= 64 on the FP64 DMMA pipe.
 //
 // Replaces accumulate_into<double> (reference src/suffstats.cpp:50-70) for one
-// accumulation tile of job.tile_rows rows (4096; fewer for small plans).  Each warp walks k-steps of 4 rows.  Lane
+// accumulation tile (4096 rows; fewer for small plans, job.tile_rows).  Each warp walks k-steps of 4 rows.  Lane
 // l = 4g + k loads the values of row k at the NB columns col(J, g), J < NB, straight
 // from HBM with coalesced streaming loads (a warp load covers 4 whole rows), subtracts
 // the range shift c, and feeds the same register as the A fragment (A[g][k]) of
@@ -133,7 +133,9 @@ __device__ int canonical_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-template <int NB, bool VEC, bool X1 = false>
+// RT = false: tiles of kTileRows rows (a compile-time bound: the loop is fully unrolled and
+// software-pipelined — measured faster); RT = true: job.tile_rows (small plans).
+template <int NB, bool VEC, bool X1 = false, bool RT = false>
 __device__ __forceinline__ void smallp_body(const TileJob& job) {
     using C = SmallP<NB, VEC, X1>;
     constexpr int U = C::U;
@@ -146,7 +148,7 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
     for (uint64_t t = job.tile_begin + blockIdx.x; t < job.tile_end; t += gridDim.x) {
         const uint32_t r = range_of_tile(job.tile_prefix, job.n_ranges, t);
         const uint64_t rs = __ldg(job.range_start + r), rc = __ldg(job.range_count + r);
-        const uint32_t TR = job.tile_rows;
+        const uint32_t TR = RT ? job.tile_rows : kTileRows;
         const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + r)) * TR;
         const uint64_t left = rs + rc - row0;
         const uint32_t rows = left < TR ? (uint32_t)left : TR;
@@ -267,31 +269,31 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
 // overrides): 3 for NB = 3..4 (<= 85 registers, 24 warps; p = 24: 4.2 -> 5.8 TB/s, p = 32:
 // 4.2 -> 5.0), 2 for NB = 5 (<= 128; p = 40: +35 %).  NB = 6 spills under a floor of 2 and
 // loses 14 %; NB >= 6 stay unbounded.
-template <int NB, bool VEC>
+template <int NB, bool VEC, bool RT>
 __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
-    smallp_body<NB, VEC>(job);
+    smallp_body<NB, VEC, false, RT>(job);
 }
-template <int NB, bool VEC, int MINB>
+template <int NB, bool VEC, int MINB, bool RT>
 __global__ void __launch_bounds__(kThreads, MINB) k_smallp_floor(TileJob job) {
-    smallp_body<NB, VEC>(job);
+    smallp_body<NB, VEC, false, RT>(job);
 }
 
-template <int NB>
+template <int NB, bool RT>
 __global__ void __launch_bounds__(kThreads) k_smallp_x1(TileJob job) {
-    smallp_body<NB, false, true>(job);
+    smallp_body<NB, false, true, RT>(job);
 }
 
-template <int NB>
+template <int NB, bool RT>
 cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, false, true>::FRAG;
-    static std::atomic<int> cached[64];
+    static std::atomic<int> cached[64];  // per instantiation (NB, RT)
     int dev = 0;
     cudaGetDevice(&dev);
     int per_sm = dev < 64 ? cached[dev].load() : 0;
     if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_smallp_x1<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_smallp_x1<NB, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp_x1<NB>, kThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp_x1<NB, RT>, kThreads, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
         if (dev < 64) cached[dev].store(per_sm);
@@ -299,23 +301,23 @@ cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
-    k_smallp_x1<NB><<<(unsigned)grid, kThreads, smem, stream>>>(job);
-    if (job.launched) *job.launched = (const void*)k_smallp_x1<NB>;
+    k_smallp_x1<NB, RT><<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    if (job.launched) *job.launched = (const void*)k_smallp_x1<NB, RT>;
     return cudaGetLastError();
 }
 
-template <int NB, bool VEC>
+template <int NB, bool VEC, bool RT>
 cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, VEC>::FRAG;
     int minb = NB == 3 || NB == 4 ? 3 : (NB == 5 ? 2 : 0);
     if (const char* env = getenv("SSTAT_K1_MINB")) minb = atoi(env);
-    void (*kern)(TileJob) = k_smallp<NB, VEC>;
+    void (*kern)(TileJob) = k_smallp<NB, VEC, RT>;
     if constexpr (NB >= 3 && NB <= 4) {
-        if (minb == 3) kern = k_smallp_floor<NB, VEC, 3>;
-        else if (minb == 2) kern = k_smallp_floor<NB, VEC, 2>;
+        if (minb == 3) kern = k_smallp_floor<NB, VEC, 3, RT>;
+        else if (minb == 2) kern = k_smallp_floor<NB, VEC, 2, RT>;
         else minb = 0;
     } else if constexpr (NB == 5) {
-        if (minb == 2) kern = k_smallp_floor<NB, VEC, 2>;
+        if (minb == 2) kern = k_smallp_floor<NB, VEC, 2, RT>;
         else minb = 0;
     } else {
         minb = 0;
@@ -342,9 +344,8 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-}  // namespace
-
-cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
+template <bool RT>
+cudaError_t launch_smallp_rt(const TileJob& job, int sms, cudaStream_t stream) {
     const uint32_t p = job.p;
     const int nb = (int)((p + 7) / 8);
     // 128-bit loads need p a multiple of 16 and a 16-byte aligned base.
@@ -354,28 +355,37 @@ cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
     // +4 / +8 %)
     if (p % 8 == 1 && p > 1 && !getenv("SSTAT_K1_NO_X1")) {
         switch (p / 8) {
-            case 1: return launch_nb_x1<1>(job, sms, stream);
-            case 2: return launch_nb_x1<2>(job, sms, stream);
-            case 3: return launch_nb_x1<3>(job, sms, stream);
+            case 1: return launch_nb_x1<1, RT>(job, sms, stream);
+            case 2: return launch_nb_x1<2, RT>(job, sms, stream);
+            case 3: return launch_nb_x1<3, RT>(job, sms, stream);
             // NB = 4 (p = 33): 136 registers, one CTA per SM — measured 18 % below the
             // occupancy-floored 5-block-row kernel, which it keeps
-            case 5: return launch_nb_x1<5>(job, sms, stream);
-            case 6: return launch_nb_x1<6>(job, sms, stream);
-            case 7: return launch_nb_x1<7>(job, sms, stream);
+            case 5: return launch_nb_x1<5, RT>(job, sms, stream);
+            case 6: return launch_nb_x1<6, RT>(job, sms, stream);
+            case 7: return launch_nb_x1<7, RT>(job, sms, stream);
             default: break;
         }
     }
     switch (nb) {
-        case 1: return launch_nb<1, false>(job, sms, stream);
-        case 2: return vec ? launch_nb<2, true>(job, sms, stream) : launch_nb<2, false>(job, sms, stream);
-        case 3: return launch_nb<3, false>(job, sms, stream);
-        case 4: return vec ? launch_nb<4, true>(job, sms, stream) : launch_nb<4, false>(job, sms, stream);
-        case 5: return launch_nb<5, false>(job, sms, stream);
-        case 6: return vec ? launch_nb<6, true>(job, sms, stream) : launch_nb<6, false>(job, sms, stream);
-        case 7: return launch_nb<7, false>(job, sms, stream);
-        case 8: return vec ? launch_nb<8, true>(job, sms, stream) : launch_nb<8, false>(job, sms, stream);
+        case 1: return launch_nb<1, false, RT>(job, sms, stream);
+        case 2: return vec ? launch_nb<2, true, RT>(job, sms, stream) : launch_nb<2, false, RT>(job, sms, stream);
+        case 3: return launch_nb<3, false, RT>(job, sms, stream);
+        case 4: return vec ? launch_nb<4, true, RT>(job, sms, stream) : launch_nb<4, false, RT>(job, sms, stream);
+        case 5: return launch_nb<5, false, RT>(job, sms, stream);
+        case 6: return vec ? launch_nb<6, true, RT>(job, sms, stream) : launch_nb<6, false, RT>(job, sms, stream);
+        case 7: return launch_nb<7, false, RT>(job, sms, stream);
+        case 8: return vec ? launch_nb<8, true, RT>(job, sms, stream) : launch_nb<8, false, RT>(job, sms, stream);
         default: return cudaErrorInvalidValue;
     }
+}
+
+}  // namespace
+
+// Full-height tiles take the kernels with the compile-time tile height; small plans' shorter
+// tiles (job.tile_rows < kTileRows) the runtime-height instances.
+cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
+    return job.tile_rows == kTileRows ? launch_smallp_rt<false>(job, sms, stream)
+                                      : launch_smallp_rt<true>(job, sms, stream);
 }
 
 }  // namespace sstat_b200

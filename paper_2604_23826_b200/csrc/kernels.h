@@ -33,10 +33,11 @@ cudaError_t launch_gather_shift(const double* base, uint64_t base_row, const uin
 // non-finite ranges (global index first_range + r) in the header.
 // The shift row: shift[r*p], or (shift == nullptr, base != nullptr) the range's first row
 // read in place from the resident shard base (absolute row base_row at base[0]).
+// chunks: the launch's cluster size = max over its ranges of fold_chunks(tiles of the range).
 cudaError_t launch_range_fold(const double* tile_partials, const uint64_t* tile_prefix, const uint64_t* range_count,
                               const double* shift, const double* base, uint64_t base_row, const uint64_t* range_start,
                               uint32_t n_ranges, uint32_t p, uint64_t first_range, double* rank_buf, uint32_t* flags,
-                              cudaStream_t stream);
+                              uint32_t chunks, cudaStream_t stream);
 
 // First non-finite value (row-major) over the flagged local ranges (flags[r] != 0);
 // min absolute linear index row*p + col lands in header[1].  No-op when none flagged.
