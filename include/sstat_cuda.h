@@ -164,7 +164,8 @@ int sstat_cuda_init(sstat_cuda_ctx** ctx, int device);
  *   sstat_cuda_generate: the member whose device holds dst;
  *   sstat_cuda_set_staging / _set_host_threads: every member (host threads default to
  *     min(16, cores) / n_gpus per member);
- *   sstat_cuda_set_stream (non-NULL) and sstat_cuda_comm_init: rejected. */
+ *   sstat_cuda_set_stream (non-NULL) and sstat_cuda_comm_init: rejected.
+ * n_gpus = 0 (devices NULL): every visible device. */
 int sstat_cuda_init_devices(sstat_cuda_ctx** ctx, int n_gpus, const int* devices);
 /* Devices a context drives: 1, or the group's n_gpus. */
 int sstat_cuda_device_count(const sstat_cuda_ctx* ctx);

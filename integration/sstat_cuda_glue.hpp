@@ -75,7 +75,9 @@ inline SuffStats make_result(const DatasetSchema& schema, PrecisionMode precisio
 }
 }  // namespace detail
 
-/// One libsstat_b200 context (one CUDA device).  Thread-safe: calls serialise per engine.
+/// One libsstat_b200 context: one CUDA device, or a device group — every GPU of the box
+/// driven from this one process (sstat_cuda_init_devices; the paper's single host process,
+/// PAPER.md:70).  Thread-safe: calls serialise per engine.
 class Engine {
 public:
     explicit Engine(int device = -1) {
@@ -84,6 +86,18 @@ public:
         if (st != SSTAT_OK) throw DeviceError(st, std::string("sstat_cuda_init: ") + sstat_status_string(st));
         ctx_.reset(c);
     }
+    /// A device group over `devices`: the plan's ranges are sharded contiguously over them and
+    /// folded in the same order — bit-identical to one device.
+    explicit Engine(const std::vector<int>& devices) {
+        sstat_cuda_ctx* c = nullptr;
+        const int st = sstat_cuda_init_devices(&c, static_cast<int>(devices.size()),
+                                               devices.empty() ? nullptr : devices.data());
+        if (st != SSTAT_OK) throw DeviceError(st, std::string("sstat_cuda_init_devices: ") + sstat_status_string(st));
+        ctx_.reset(c);
+    }
+    /// Every visible GPU as one group (an empty list: sstat_cuda_init_devices(ctx, 0, NULL)).
+    static Engine all_devices() { return Engine(std::vector<int>{}); }
+    int device_count() const { return sstat_cuda_device_count(get()); }
     sstat_cuda_ctx* get() const { return ctx_.get(); }
 
     /// Multi-GPU: one process per GPU; `id` from sstat_cuda_nccl_unique_id on rank 0,

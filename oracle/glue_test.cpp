@@ -13,7 +13,8 @@
 //   3. the GPU as run_reduction's per_chunk (include/sstat/reduce.hpp:70-146);
 //   4. error mapping: non-finite -> ReductionError(range, message), bad file -> FormatError,
 //      partition mismatch -> std::invalid_argument, accumulate_chunk -> NonFiniteError;
-//   5. sidecar round trip (src/suffstats.cpp:190-277) of a GPU result.
+//   5. sidecar round trip (src/suffstats.cpp:190-277) of a GPU result;
+//   8. the device-group engine (one process, several devices) through the same glue call.
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -191,6 +192,21 @@ int main() {
                 worst = std::max(worst, std::fabs(cm_gpu.m2.at(j, k) - cm_cpu.m2.at(j, k)) / sc);
             }
         CHECK(worst <= 1e-12);
+    }
+
+    // 8. the device-group engine (sstat_cuda_init_devices): the reference's single-process
+    //    dataset_suffstats(path, schema, plan) over every member — {0} and {0, 0, 0} (three
+    //    members on one GPU: per-member file feeders, peer-copy exchange, device fold over three
+    //    rank buffers) give the single-device bits, in both modes
+    {
+        for (const std::vector<int>& devs : {std::vector<int>{0}, std::vector<int>{0, 0, 0}}) {
+            cuda::Engine group(devs);
+            CHECK(group.device_count() == static_cast<int>(devs.size()));
+            const SuffStats g_exact = cuda::dataset_suffstats(group, bin, schema, plan, nullptr, SSTAT_FLAG_REFEXACT);
+            CHECK(g_exact == cpu);
+            const SuffStats g_fast = cuda::dataset_suffstats(group, bin, schema, plan);
+            CHECK(g_fast == gpu);
+        }
     }
 
     // 5. sidecar round trip of the GPU result

@@ -441,6 +441,10 @@ struct Plan {
 // 592 slots) — the largest power of two >= kMinTileRows giving at least kFillTiles tiles.
 // A function of the global plan alone: every rank and GPU count cuts the same tiles.
 uint64_t smallp_tile_rows(const Plan& P) {
+    if (const char* env = getenv("SSTAT_K1_TILE_ROWS")) {  // experiment knob: a fixed height (multiple of 32)
+        const uint64_t tr = strtoull(env, nullptr, 10);
+        if (tr >= 32 && tr <= kTileRows && tr % 32 == 0) return tr;
+    }
     if (P.total / kTileRows >= kFillTiles) return kTileRows;  // sum of ceil(count / TR) >= total / TR
     uint64_t TR = kTileRows;
     for (; TR > kMinTileRows; TR /= 2) {
@@ -1696,10 +1700,16 @@ int sstat_cuda_init(sstat_cuda_ctx** out, int device) {
 }
 
 int sstat_cuda_init_devices(sstat_cuda_ctx** out, int n_gpus, const int* devices) {
-    if (!out || n_gpus < 1 || !devices) return SSTAT_ERR_INVALID;
+    if (!out || n_gpus < 0 || (n_gpus > 0 && !devices)) return SSTAT_ERR_INVALID;
     *out = nullptr;
     const int n = device_count();
     if (n == 0) return SSTAT_ERR_CUDA;
+    std::vector<int> all;
+    if (n_gpus == 0) {  // every visible device
+        for (int i = 0; i < n; ++i) all.push_back(i);
+        n_gpus = n;
+        devices = all.data();
+    }
     bool distinct = true;
     for (int i = 0; i < n_gpus; ++i) {
         if (devices[i] < 0 || devices[i] >= n) return SSTAT_ERR_INVALID;

@@ -1,9 +1,13 @@
 // fold.cuh — the per-range fold (K3a) device code.  Blocks of 256 threads.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace sstat_b200 {
+
+namespace cg = cooperative_groups;
 
 // Tile partials come from the previous kernel; read them through L2 (ld.global.cg).
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
@@ -11,9 +15,9 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // Tile folds of one range run kTileLanes interleaved lanes per entry: lane q sums tiles
 // t0+q, t0+q+kTileLanes, ... (kFoldInFlight loads in flight, masked tails instead of a serial
 // remainder loop), then the lanes are added 0..kTileLanes-1.  A fixed function of the range's
-// tile partials; blocks are kTileLanes x 32 threads.  32 lanes x 16 loads in flight keep a
-// range of ~2000 small-plan tiles (C1: 1e6 rows in 512-row tiles) to four L2 round trips.
-constexpr int kTileLanes = 32;
+// tile partials; blocks are kTileLanes x 32 threads (512: four per SM, so C2's 480 fold blocks
+// run in one wave — 1024-thread blocks measured 2x slower there).
+constexpr int kTileLanes = 16;
 constexpr int kFoldInFlight = 16;
 __device__ __forceinline__ double fold_tiles_lane(const double* __restrict__ tp, uint64_t E, uint64_t e, uint64_t t0,
                                                   uint64_t t1, int q) {
@@ -116,16 +120,16 @@ __device__ inline void fold_range_block(const double* __restrict__ tp, uint64_t 
     if (k == 0) {
         // 2. CTA 0: the chunk partials in order 0..C-1 (remote ones through DSMEM)
         if constexpr (CLUSTER) {
+            cg::cluster_group cluster = cg::this_cluster();
             for (uint64_t i = threadIdx.x; i < n_mine; i += blockDim.x) {
+                double v[kMaxChunks];
+#pragma unroll
+                for (uint32_t kk = 1; kk < kMaxChunks; ++kk)  // all remote loads in flight, then the adds in order
+                    v[kk] = kk < C ? *cluster.map_shared_rank(cp + i, kk) : 0.0;
                 double S = cp[i];
-                for (uint32_t kk = 1; kk < C; ++kk) {
-                    uint64_t raddr;
-                    const uint64_t laddr = (uint64_t)__cvta_generic_to_shared(cp + i);
-                    asm volatile("mapa.shared::cluster.u64 %0, %1, %2;" : "=l"(raddr) : "l"(laddr), "r"(kk));
-                    double v;
-                    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "l"(raddr) : "memory");
-                    S += v;
-                }
+#pragma unroll
+                for (uint32_t kk = 1; kk < kMaxChunks; ++kk)
+                    if (kk < C) S += v[kk];
                 cp[i] = S;
             }
             __syncthreads();
