@@ -239,8 +239,9 @@ __global__ void __launch_bounds__(256) k_comoment_merge(const double* __restrict
     double* delta = sm + p;
     const uint64_t E = partial_len(p), NP = E - p;
     double* m2 = out + p;
-    if (blockIdx.x == 0 && threadIdx.x < (unsigned)world * kHdr)  // append the rank headers
-        out[E + threadIdx.x] = buf[(threadIdx.x / kHdr) * rank_stride + threadIdx.x % kHdr];
+    if (blockIdx.x == 0)  // append the rank headers
+        for (uint32_t h = threadIdx.x; h < (uint32_t)world * kHdr; h += blockDim.x)
+            out[E + h] = buf[(h / kHdr) * rank_stride + h % kHdr];
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // this thread's M2 entry
     const bool has = i < NP;
     uint32_t j = 0, k = 0;
