@@ -210,3 +210,39 @@ def test_fold_range_partials_resume_equals_reference(oracle):
     assert np.array_equal(bits(got.sums), bits(want[1])) and np.array_equal(bits(got.cross), bits(want[2]))
     with pytest.raises(ValueError):
         fold_range_partials(np.array(parts[:-1]), schema, plan)
+
+
+def test_partition_arrays_follow_in_place_edits():
+    """Partition's cached C-ABI arrays are keyed on the ranges' contents (a mutation counter on
+    the list), so replacing a middle RowRange in place, appending, or reassigning the list is seen
+    (keyed on (id, len, last) it reused stale arrays)."""
+    from paper_2604_23826_b200 import RowRange, plan_partitions
+
+    part = plan_partitions(100, 10)
+    s0, c0 = part.arrays()
+    assert list(s0[:3]) == [0, 10, 20]
+    part.ranges[1] = RowRange(10, 5)
+    s1, c1 = part.arrays()
+    assert list(c1[:3]) == [10, 5, 10]
+    part.ranges.append(RowRange(100, 7))
+    assert part.arrays()[1][-1] == 7 and len(part.arrays()[0]) == 11
+    part.ranges = [RowRange(0, 3)]
+    assert list(part.arrays()[1]) == [3]
+    a0 = part.addresses()
+    assert part.addresses() == a0  # unchanged plan: the same cached arrays
+
+
+def test_array_width_checked_against_schema():
+    """An (n, 12) array under an 11-column schema is the reference's SchemaMismatchError wrapped in
+    ReductionError for range 0 (check_chunk, suffstats.cpp:33-36), not a coverage error."""
+    from paper_2604_23826_b200 import ReductionError, SchemaMismatchError
+    from paper_2604_23826_b200.sstat import _check_width
+
+    _check_width(np.zeros((5, 11)), 11)
+    _check_width(np.zeros(44), 11)
+    with pytest.raises(ReductionError) as e:
+        _check_width(np.zeros((5, 12)), 11)
+    assert e.value.range_index() == 0 and isinstance(e.value.cause, SchemaMismatchError)
+    assert "chunk has 12 columns, schema has 11" in str(e.value)
+    with pytest.raises(ReductionError):
+        _check_width(np.zeros(45), 11)

@@ -36,6 +36,20 @@ for name, n, p, kind, n_int in (("C1", 1_000_000, 9, 1, 0), ("C2", 100_000_000, 
             t = eng.last_timings
             extra = f" K1 {t.kernel_seconds * 1e6:.1f} us folds {t.fold_seconds * 1e6:.1f} us kernel {t.kernel.decode()}"
         print(f"{name} timings={'on ' if timed else 'off'} step {ms * 1e3:.1f} us{extra}", flush=True)
+    # the practical read floor at this size: a plain device-wide read of the same bytes
+    # (torch.sum over the tensor), timed the same way
+    for _ in range(5):
+        D.sum()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(K):
+        D.sum()
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / K
+    print(f"{name} read floor (torch.sum of the {n * p * 8 / 1e6:.0f} MB): {ms * 1e3:.1f} us "
+          f"= {n * p * 8 / ms / 1e9 * 1e3 / 1e3:.2f} TB/s", flush=True)
     del D
     eng.close()
     torch.cuda.empty_cache()
