@@ -516,7 +516,7 @@ def run_ours(args):
         t5, r5 = device_timed(step5, k5)
         k5_s = max_over_ranks(sum(kern5[-k5:]) / k5)
         flops = nq * C5_P * (C5_P + 2)
-        traffic, tsrc = traffic_of("k_widep_wg")
+        traffic, tsrc = traffic_of("k_widep")
         c5 = {"value": rows5 / t5, "unit": "rows/s", "ms_per_step": t5 * 1e3, "steps": k5, "global_rows": rows5,
               "rows_per_gpu": nq, "p": C5_P, "ranges": len(pl5.partition.ranges),
               "tflops": rows5 * C5_P * (C5_P + 2) / t5 / 1e12, "result_sha256": sha_bits(r5),

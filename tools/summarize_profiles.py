@@ -1,46 +1,71 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) and an ncu
---set full report into profiles/<tag>_*.  Usage:
-    python tools/summarize_profiles.py <tag> gpurun_out/launches.csv gpurun_out/k1_full.ncu-rep
+"""Summarise ncu output into profiles/ (tracked):
+  * a launch list (ncu --metrics gpu__time_duration.sum[,dram__bytes_*] --csv): per-kernel launches,
+    average duration, share of the profiled time, DRAM bytes per launch;
+  * --set full reports: the key metrics of each captured launch, and (--traffic key) the captured
+    launch's DRAM bytes into profiles/traffic.json for bench.py's roofline.traffic.
+Usage:
+    python tools/summarize_profiles.py launches <out.md> <launches.csv> "<command>"
+    python tools/summarize_profiles.py full <out.md> <report.ncu-rep> "<title>" [--traffic key "workload"]
 """
 import csv
+import json
+import os
 import subprocess
 import sys
 from collections import defaultdict
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__bytes.sum.per_second",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "gpc__cycles_elapsed.avg.per_second",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
-    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "launch__cluster_dim_x", "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__ops_path_tensor_src_fp64.sum",
-    "lts__t_bytes.sum", "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
-    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "lts__t_bytes.sum", "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__t_bytes.sum",
 ]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
-def launches(path):
+def launch_table(path):
     rows = list(csv.reader(l for l in open(path) if not l.startswith("==")))
     hdr = rows[0]
-    i_name, i_val = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    agg = defaultdict(list)
+    i_id, i_name, i_m, i_u, i_v = (hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Unit",
+                                                           "Metric Value"))
+    per = defaultdict(dict)  # (id, kernel) -> metric -> value
     for r in rows[1:]:
-        agg[r[i_name].replace("(anonymous namespace)::", "").split("(")[0]].append(float(r[i_val].replace(",", "")))
-    tot = sum(sum(v) for v in agg.values())
-    out = ["| kernel | launches | total ms | avg us | share |", "|---|---:|---:|---:|---:|"]
-    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        out.append(f"| `{k}` | {len(v)} | {sum(v) / 1e6:.3f} | {sum(v) / len(v) / 1e3:.1f} | {100 * sum(v) / tot:.1f}% |")
+        if len(r) != len(hdr):
+            continue
+        v = float(r[i_v].replace(",", "")) * SCALE.get(r[i_u], 1)
+        per[(r[i_id], r[i_name].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0].replace("void ", ""))][r[i_m]] = v
+    agg = defaultdict(list)
+    for (_, k), m in per.items():
+        agg[k].append(m)
+    tot = sum(m.get("gpu__time_duration.sum", 0) for v in agg.values() for m in v)
+    out = ["| kernel | launches | avg us | share | DRAM read / launch | DRAM write / launch |",
+           "|---|---:|---:|---:|---:|---:|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(m.get("gpu__time_duration.sum", 0) for m in kv[1])):
+        t = sum(m.get("gpu__time_duration.sum", 0) for m in v)
+        rd = sum(m.get("dram__bytes_read.sum", 0) for m in v) / len(v)
+        wr = sum(m.get("dram__bytes_write.sum", 0) for m in v) / len(v)
+        out.append(f"| `{k}` | {len(v)} | {t / len(v) / 1e3:.1f} | {100 * t / tot:.1f}% | {rd / 1e9:.4f} GB | "
+                   f"{wr / 1e9:.4f} GB |")
     return "\n".join(out)
 
 
-def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
-    hdr, units = rows[0], rows[1]
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    return rows[0], rows[1], rows[2:]
+
+
+def full_table(rep):
+    hdr, units, launches = raw(rep)
     out = []
-    for vals in rows[2:]:
+    for vals in launches:
         name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
         out.append(f"### `{name}`\n\n| metric | value | unit |\n|---|---:|---|")
         for i, h in enumerate(hdr):
@@ -49,28 +74,34 @@ def full(path):
     return "\n".join(out)
 
 
-def traffic(rep):
-    """dram read/write bytes of the captured launch (for bench.py's roofline.traffic)."""
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+def update_traffic(rep, key, workload, source):
+    hdr, units, launches = raw(rep)
+    vals = launches[0]
 
     def get(name):
         i = hdr.index(name)
-        return float(vals[i].replace(",", "")) * scale[units[i]]
+        return float(vals[i].replace(",", "")) * SCALE[units[i]]
 
-    return {"dram_read_bytes": get("dram__bytes_read.sum"), "dram_write_bytes": get("dram__bytes_write.sum")}
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    tr = json.load(open(path)) if os.path.exists(path) else {}
+    tr[key] = {"dram_read_bytes": get("dram__bytes_read.sum"), "dram_write_bytes": get("dram__bytes_write.sum"),
+               "duration_ms": get("gpu__time_duration.sum") / 1e6 if units[hdr.index("gpu__time_duration.sum")] == "ns"
+               else None, "source": source, "workload": workload}
+    json.dump(tr, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":
-    tag, lc, rep = sys.argv[1:4]
-    with open(f"profiles/{tag}_launches.md", "w") as f:
-        f.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none, cold & serialised)\n\n")
-        f.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py "
-                "--steps 2 --warmup 3 --no-e2e --no-cpu --no-next`\n\n")
-        f.write(launches(lc) + "\n")
-    with open(f"profiles/{tag}_k1_full.md", "w") as f:
-        f.write(f"# {tag}: ncu --set full of the accumulate kernel (one launch, C2 1e8 x 16)\n\n")
-        f.write(full(rep) + "\n")
-    print(open(f"profiles/{tag}_launches.md").read())
+    mode, out = sys.argv[1], sys.argv[2]
+    if mode == "launches":
+        csv_path, cmd = sys.argv[3], sys.argv[4]
+        with open(out, "w") as f:
+            f.write(f"# ncu launch list (--clock-control none: cold, serialised launches)\n\nCommand: `{cmd}`\n\n")
+            f.write(launch_table(csv_path) + "\n")
+    else:
+        rep, title = sys.argv[3], sys.argv[4]
+        with open(out, "w") as f:
+            f.write(f"# {title}\n\n" + full_table(rep) + "\n")
+        if "--traffic" in sys.argv:
+            i = sys.argv.index("--traffic")
+            update_traffic(rep, sys.argv[i + 1], sys.argv[i + 2], os.path.relpath(out, ROOT))
+    print(open(out).read())
