@@ -46,6 +46,8 @@ struct TileJob {
     cudaEvent_t fork, join;
     const void** launched;         // (optional) receives the accumulate kernel the launcher chose
     uint32_t tile_rows;            // K1: rows per tile of this plan (smallp_tile_rows)
+    uint32_t shift_in_place;       // K1 runtime-height instances, shift == nullptr: the shift row is
+                                   // the range's first row read from base (a resident shard)
 };
 
 // Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).

@@ -654,6 +654,7 @@ bool rows_aligned16(const double* base, uint64_t base_row, const uint64_t* start
 struct Local {
     bool refexact = false, comoments = false, shift = false;
     bool graphable = false;  // one GPU, resident K1 pass: folds and read-back are in the graph
+    bool hdr_first = false;  // graph read-back laid out [header | result] (one-range plans)
     bool scanned = false;    // the non-finite scan already ran for this rank
     double* rank_buf = nullptr;
     uint64_t rank_stride = 0;  // kHdr + lmax * E doubles
@@ -813,10 +814,16 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
         CUDA_TRY(c->d_result.reserve((E + kHdr) * 8));  // K3b appends the rank header
         const double* base = static_cast<const double*>(src->ptr);
         // timed = the graph records the K1 / fold events (each external event node costs ~5 us of
-        // replay, so calls without timings replay a graph without them)
+        // replay, so calls without timings replay a graph without them).  small = a plan cut into
+        // short tiles (smallp_tile_rows): K1 and K3a read each range's shift row in place, so the
+        // gather kernel drops out; one_range: K3b (a copy of one partial) drops out too.
         const bool timed = tm != nullptr;
+        const bool small = TR != kTileRows;
+        const bool one_range = P.R == 1;
+        st.hdr_first = one_range;
         const std::vector<uint64_t> key = {
             (uint64_t)(uintptr_t)base, src->first_row, p, L, nt, E, P.r0, shift, (uint64_t)(uintptr_t)s, timed, TR,
+            one_range,
             c->d_meta.gen, c->d_tiles.gen, c->d_rank.gen, c->d_flags.gen, c->d_shift.gen, c->d_result.gen,
             (uint64_t)(uintptr_t)c->h_result.p, (uint64_t)(uintptr_t)c->d_meta.p, (uint64_t)(uintptr_t)c->d_tiles.p,
             (uint64_t)(uintptr_t)c->d_rank.p, (uint64_t)(uintptr_t)c->d_shift.p, (uint64_t)(uintptr_t)c->d_result.p};
@@ -828,7 +835,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
             cudaGraph_t g = nullptr;
             try {
                 const cudaStream_t cs = c->cap;
-                if (shift)
+                if (shift && !small)
                     CUDA_TRY(launch_gather_shift(base, src->first_row, d_starts, d_counts, (uint32_t)L, p,
                                                  c->d_shift.as<double>(), cs));
                 if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[0], cs, cudaEventRecordExternal));
@@ -838,7 +845,8 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                 j.range_start = d_starts;
                 j.range_count = d_counts;
                 j.tile_prefix = d_prefix;
-                j.shift = d_shift;
+                j.shift = small ? nullptr : d_shift;
+                j.shift_in_place = small && shift;
                 j.n_ranges = (uint32_t)L;
                 j.p = p;
                 j.tile_begin = 0;
@@ -848,12 +856,19 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
                 j.tile_rows = (uint32_t)TR;
                 CUDA_TRY(launch_smallp(j, c->sms, cs));
                 if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[1], cs, cudaEventRecordExternal));
-                CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, d_shift, nullptr, 0, d_starts,
-                                           (uint32_t)L, p, P.r0, rank_buf, d_flags, fold_k, cs));
-
-                CUDA_TRY(launch_final_fold(rank_buf, rank_stride, P.R, 1, p, 0u, false, c->d_result.as<double>(), cs));
-                if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
-                CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + kHdr) * 8, cudaMemcpyDeviceToHost, cs));
+                CUDA_TRY(launch_range_fold(c->d_tiles.as<double>(), d_prefix, d_counts, small ? nullptr : d_shift,
+                                           small && shift ? base : nullptr, src->first_row, d_starts, (uint32_t)L, p,
+                                           P.r0, rank_buf, d_flags, fold_k, cs));
+                if (one_range) {
+                    // one range: the fold of one partial is the partial itself (K3a adds + 0.0 like the
+                    // fold would), so the read-back takes the rank buffer [header | partial] directly
+                    if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
+                    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, rank_buf, (E + kHdr) * 8, cudaMemcpyDeviceToHost, cs));
+                } else {
+                    CUDA_TRY(launch_final_fold(rank_buf, rank_stride, P.R, 1, p, 0u, false, c->d_result.as<double>(), cs));
+                    if (timed) CUDA_TRY(cudaEventRecordWithFlags(c->ev[4], cs, cudaEventRecordExternal));
+                    CUDA_TRY(cudaMemcpyAsync(c->h_result.p, c->d_result.p, (E + kHdr) * 8, cudaMemcpyDeviceToHost, cs));
+                }
             } catch (...) {
                 cudaStreamEndCapture(c->cap, &g);
                 if (g) cudaGraphDestroy(g);
@@ -1112,6 +1127,12 @@ void run_fold(sstat_cuda_ctx* c, const sstat_cuda_source* src, const Plan& P, co
     double* hres = c->h_result.as<double>();
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
+    if (st.graphable && st.hdr_first) {  // [header | result] -> [result | header]
+        double hdr[kHdr];
+        std::memcpy(hdr, hres, sizeof hdr);
+        std::memmove(hres, hres + kHdr, E * 8);
+        std::memcpy(hres + E, hdr, sizeof hdr);
+    }
     if (!st.scanned && world == 1 && L > 0) {
         uint64_t flagged;
         std::memcpy(&flagged, hres + E, 8);

@@ -140,7 +140,7 @@ __device__ inline void fold_range_block(const double* __restrict__ tp, uint64_t 
             const double cj = c ? c[i] : 0.0;
             ssum[i] = S;
             sc[i] = cj;
-            if (lead) out[i] = S + n * cj;
+            if (lead) out[i] = (S + n * cj) + 0.0;  // + 0.0: a partial is never -0.0, like the reference's
             if (lead && (!isfinite(S) || !isfinite(cj))) {
                 *flag = 1;
                 atomicMin(reinterpret_cast<unsigned long long*>(rank_hdr), (unsigned long long)global_range);
@@ -155,7 +155,7 @@ __device__ inline void fold_range_block(const double* __restrict__ tp, uint64_t 
                 unpack_index(p, (uint32_t)(e - p), j, kk);
                 S = ((S + sc[j] * ssum[kk]) + sc[kk] * ssum[j]) + (n * sc[j]) * sc[kk];
             }
-            out[e] = S;
+            out[e] = S + 0.0;
         }
     }
     if constexpr (CLUSTER) {  // CTA 0's remote reads are done before any CTA of the cluster exits

@@ -156,7 +156,9 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
 
         // shift row c of this range (the gathered table; reading it in place from the shard
         // costs this kernel 16 registers and 1.6% of its bandwidth — measured)
-        const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p : nullptr;
+        const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p
+                             : (RT && job.shift_in_place && rc) ? job.base + (rs - job.base_row) * p
+                                                               : nullptr;
         double c[NB];
 #pragma unroll
         for (int J = 0; J < NB; ++J) {

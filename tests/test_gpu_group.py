@@ -288,3 +288,34 @@ def test_reader_source(engine):
         e.dataset_suffstats(RowReader(broken, n), schema(p), pl)
     assert e.dataset_suffstats(RowReader(point, n), schema(p), pl).bit_equal(want)
     e.close()
+
+
+@pytest.mark.parametrize("n,chunk", [(1_000_000, 1 << 20), (300_000, 100_000), (5_000, 1 << 20)])
+def test_small_plans_match_the_reference(engine, oracle, n, chunk):
+    """Plans too small for 4096-row tiles (C1's shape and smaller): K1 cuts shorter tiles and reads
+    each range's shift row in place, K3a folds long ranges over a cluster, a one-range plan skips
+    K3b — the fast path stays within tolerance of the reference order and bit-exact on the integer
+    columns; an all -0.0 column gives +0.0 sums like the reference's fold from +0.0; a non-finite
+    value reports the single-range error."""
+    from paper_2604_23826_b200 import ReductionError
+
+    torch = torch_mod()
+    p = 9
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 1, 42, 1.0, 0, 0, n, p)  # column 0 = row number (integer)
+    D[:, 5] = -0.0
+    pl = plan(n, chunk)
+    fast = engine.dataset_suffstats(D, schema(p), pl)
+    X = D.cpu().numpy()
+    s, c = oracle.plan_partitions(n, chunk)
+    _, ws, wS = oracle.run_reduction(X, p, s, c, 8)
+    assert np.array_equal(bits(fast.sums[[0, 5]]), bits(ws[[0, 5]]))
+    assert bits(fast.sums[5:6])[0] == 0  # +0.0
+    assert cs_err(fast.cross, wS, p) <= 1e-12 or n * (n + 1) * (2 * n + 1) // 6 > 2**53
+    exact = engine.dataset_suffstats(D, schema(p), pl, flags=2)
+    assert np.array_equal(bits(exact.cross), bits(wS)) and np.array_equal(bits(exact.sums), bits(ws))
+    D[n // 3, 7] = float("nan")
+    with pytest.raises(ReductionError) as e:
+        engine.dataset_suffstats(D, schema(p), pl)
+    assert e.value.cause.row() == n // 3 and e.value.cause.column() == 7
+    assert e.value.range_index() == (n // 3) // chunk
