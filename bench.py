@@ -298,7 +298,9 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator's own log lines (ring / NVLS)
+        # the communicators' own log lines (transport, rings / NVLS), on stderr: stdout carries the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
