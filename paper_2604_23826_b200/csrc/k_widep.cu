@@ -39,6 +39,8 @@
 // SSTAT_DEBUG prints the plans.
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
+#include <utility>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -66,7 +68,7 @@ struct WideGeom {
     uint32_t R;              // rectangle side in 8-column blocks (nr = ceil(nb / R))
     uint32_t csize;          // CTAs per cluster (K)
     uint32_t cpt;            // clusters per tile (m); n_groups == K * m
-    const uint32_t* items;   // device [n_groups][consumers]: idle<<28 | I<<14 | J
+    const uint32_t* items;   // device [n_groups][consumers]: item words (item_word)
     // dynamic split with a concurrent second launch (nullptr = static unit order): both
     // launches claim work from one 64-bit word — role 0 (clustered, cpt == 1) whole tiles
     // from the bottom, role 1 (cluster-less) (tile, group) units from the top
@@ -202,6 +204,55 @@ __device__ __forceinline__ void kmma(double (&acc)[R * R][2], const double (&r)[
         for (int b = 0; b < R; ++b) dmma_8x8x4(acc[a * R + b][0], acc[a * R + b][1], r[a], r[R + b]);
 }
 
+// ---- work items ----
+// An item is one consumer warp's share of a tile: which 8-column blocks its fragments hold and
+// which block products it accumulates, as one straight-line program per KIND:
+//   kRect      R x R rectangle of the R-block groups I < J (I == J: a diagonal rectangle whose
+//              mirrored blocks are computed and dropped)
+//   kRectCol3  R x (R-1): groups I x J without J's last block
+//   kRectRow3  (R-1) x R: groups I x J without I's last block
+//   kDiagCol   diagonal group I's upper blocks (a <= b) + the column strip (I's blocks x block J)
+//   kDiagRow   diagonal group I's upper blocks + the row strip (block J x I's blocks)
+// Word: idle << 28 | kind << 24 | sums << 23 | I << 11 | J (J: a group for the rectangle
+// kinds, an absolute block for the strips).  `sums`: the item adds the column sums of its
+// J fragments (rectangles) or of all its fragments (diagonal kinds).
+enum : uint32_t { kRect = 0, kRectCol3 = 1, kRectRow3 = 2, kDiagCol = 3, kDiagRow = 4 };
+constexpr uint32_t kSumsBit = 1u << 23;
+__host__ __device__ constexpr uint32_t item_word(uint32_t kind, uint32_t I, uint32_t J, bool sums) {
+    return (kind << 24) | (sums ? kSumsBit : 0u) | (I << 11) | J;
+}
+
+template <int R, uint32_t KIND>
+struct Prog {
+    static constexpr bool DIAG = KIND == kDiagCol || KIND == kDiagRow;
+    static constexpr int NI = KIND == kRectRow3 ? R - 1 : R;      // fragments of group I
+    static constexpr int NJ = DIAG ? 1 : (KIND == kRectCol3 ? R - 1 : R);
+    static constexpr int NF = NI + NJ;
+    static constexpr int NDIAG = R * (R + 1) / 2;
+    static constexpr int NACC = DIAG ? NDIAG + R : NI * NJ;
+    static constexpr int NSUM = DIAG ? NF : NJ;                    // fragments whose sums it adds
+    static constexpr int SUM0 = DIAG ? 0 : NI;                     // ... starting at this one
+    // product i: fragment fa(i) as the A operand (rows of the block pair), fb(i) as B
+    __host__ __device__ static constexpr int fa(int i) {
+        if (!DIAG) return i / NJ;
+        if (i < NDIAG) {
+            int a = 0, left = i;
+            while (left >= R - a) left -= R - a, ++a;
+            return a;
+        }
+        return KIND == kDiagCol ? i - NDIAG : NI;
+    }
+    __host__ __device__ static constexpr int fb(int i) {
+        if (!DIAG) return NI + i % NJ;
+        if (i < NDIAG) {
+            int a = 0, left = i;
+            while (left >= R - a) left -= R - a, ++a;
+            return a + left;
+        }
+        return KIND == kDiagCol ? NI : i - NDIAG;
+    }
+};
+
 constexpr uint64_t kNoUnit = ~0ull;
 
 // The claim word: low 32 bits = tiles taken by role 0 from the bottom (a prefix [0, a)),
@@ -257,12 +308,12 @@ __device__ __forceinline__ uint64_t acquire_unit(const TileJob& job, const WideG
     return *(volatile uint64_t*)slot;
 }
 
-// One ring stage of SROWS rows: a straight-line program with the next k-step's fragment
+// One ring stage of SROWS rows of an R x R rectangle (the plain plans): a straight-line program with the next k-step's fragment
 // loads issued under the current k-step's DMMAs.  The slot is released (release()) as soon as
 // the last k-step's fragments have been consumed by its shift subtraction — before that
 // k-step's DMMAs — so the producers can refill it a k-step earlier.
 template <int SROWS, int R, bool SUMS, class Release>
-__device__ __forceinline__ void consume_stage(double (&acc)[R * R][2], double (&sums)[R], const double* st,
+__device__ __forceinline__ void consume_stage_rect(double (&acc)[R * R][2], double (&sums)[R], const double* st,
                                               uint32_t pitch, int colI, int colJ, const double (&cw)[2 * R],
                                               Release&& release) {
     constexpr int Q = SROWS / 4;
@@ -283,13 +334,128 @@ __device__ __forceinline__ void consume_stage(double (&acc)[R * R][2], double (&
     }
 }
 
+// One ring stage of SROWS rows of item program P: a straight-line program with the next
+// k-step's fragment loads issued under the current k-step's DMMAs.  The slot is released
+// (release()) as soon as the last k-step's fragments have been consumed by its shift subtraction
+// — before that k-step's DMMAs — so the producers can refill it a k-step earlier.
+// Fragment f reads column colI + 8f (f < NI) or colJ + 8(f - NI); DADD shares the FP64 pipe with
+// DMMA (profiles/r01_fp64_mix_probe.log), so only the items marked `sums` add column sums.
+template <class P>
+__device__ __forceinline__ void load_frags_p(double (&r)[P::NF], const double* st, int colI, int colJ) {
+#pragma unroll
+    for (int f = 0; f < P::NF; ++f) r[f] = st[f < P::NI ? colI + 8 * f : colJ + 8 * (f - P::NI)];
+}
+template <class P, bool SUMS>
+__device__ __forceinline__ void kprep_p(double (&sums)[P::NSUM], double (&r)[P::NF], const double (&cw)[P::NF]) {
+#pragma unroll
+    for (int f = 0; f < P::NF; ++f) r[f] -= cw[f];
+    if (SUMS) {
+#pragma unroll
+        for (int k = 0; k < P::NSUM; ++k) sums[k] += r[P::SUM0 + k];
+    }
+}
+// (the operand indices are forced to compile-time constants: a runtime index into the
+// fragment registers would put them in local memory)
+template <class P, int... Is>
+__device__ __forceinline__ void kmma_seq(double (&acc)[P::NACC][2], const double (&r)[P::NF],
+                                         std::integer_sequence<int, Is...>) {
+    (dmma_8x8x4(acc[Is][0], acc[Is][1], r[std::integral_constant<int, P::fa(Is)>::value],
+                r[std::integral_constant<int, P::fb(Is)>::value]),
+     ...);
+}
+template <class P>
+__device__ __forceinline__ void kmma_p(double (&acc)[P::NACC][2], const double (&r)[P::NF]) {
+    kmma_seq<P>(acc, r, std::make_integer_sequence<int, P::NACC>{});
+}
+template <class P, class Blk, int... Is>
+__device__ __forceinline__ void write_items_seq(double* out, uint32_t p, uint32_t nb, int g, int kk,
+                                                const double (&acc)[P::NACC][2], Blk&& blk,
+                                                std::integer_sequence<int, Is...>) {
+    auto one = [&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        const uint32_t A = blk(P::fa(i)), B = blk(P::fb(i));
+        if (A <= B && B < nb) write_block(out, p, A, B, g, kk, acc[i]);
+    };
+    (one(std::integral_constant<int, Is>{}), ...);
+}
+template <int SROWS, class P, bool SUMS, class Release>
+__device__ __forceinline__ void consume_stage_p(double (&acc)[P::NACC][2], double (&sums)[P::NSUM], const double* st,
+                                              uint32_t pitch, int colI, int colJ, const double (&cw)[P::NF],
+                                              Release&& release) {
+    constexpr int Q = SROWS / 4;
+    double ra[P::NF], rb[P::NF];
+    load_frags_p<P>(ra, st, colI, colJ);
+#pragma unroll
+    for (int q = 0; q < Q; q += 2) {
+        if (q + 1 < Q) load_frags_p<P>(rb, st + 4 * (q + 1) * pitch, colI, colJ);
+        kprep_p<P, SUMS>(sums, ra, cw);
+        if (q + 1 == Q) release();
+        kmma_p<P>(acc, ra);
+        if (q + 2 < Q) load_frags_p<P>(ra, st + 4 * (q + 2) * pitch, colI, colJ);
+        if (q + 1 < Q) {
+            kprep_p<P, SUMS>(sums, rb, cw);
+            if (q + 2 == Q) release();
+            kmma_p<P>(acc, rb);
+        }
+    }
+}
+
+// One unit (tile, group) of item program P for this warp: the stages, then the epilogue — the
+// item's disjoint canonical entries of the tile partial.  Advances the ring position.
+template <int SROWS, int R, class P, bool SUMS, class Wait, class Release>
+__device__ __forceinline__ void run_item(const TileJob& job, const WideGeom& geo, const UnitInfo& ui, uint32_t I,
+                                         uint32_t J, int g, int kk, const double* sm, uint32_t slot_elems,
+                                         uint32_t& slot, uint32_t& ph, Wait&& wait, Release&& release) {
+    const uint32_t p = geo.p, pitch = geo.pitch, nb = geo.nb;
+    // the 8-column block of fragment f
+    auto blk = [&](int f) -> uint32_t {
+        return f < P::NI ? R * I + f : (P::DIAG ? J : R * J + (f - P::NI));
+    };
+    const int colI = (int)(8 * R * I) + g, colJ = (int)(8 * (P::DIAG ? J : R * J)) + g;
+    double cw[P::NF];
+#pragma unroll
+    for (int f = 0; f < P::NF; ++f) {
+        const int col = (int)(8 * blk(f)) + g;
+        cw[f] = (col < (int)p && job.shift != nullptr) ? job.shift[(uint64_t)ui.r * p + col] : 0.0;
+    }
+    double acc[P::NACC][2], sums[P::NSUM];
+#pragma unroll
+    for (int i = 0; i < P::NACC; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < P::NSUM; ++i) sums[i] = 0.0;
+    const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
+    for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
+        wait(slot, ph);
+        const double* st = sm + slot * slot_elems + kk * pitch;
+        const uint32_t s0 = slot;
+        consume_stage_p<SROWS, P, SUMS>(acc, sums, st, pitch, colI, colJ, cw, [&]() { release(s0); });
+        if (++slot == geo.ring) slot = 0, ph ^= 1;
+    }
+    double* out = job.tile_partials + ui.t * partial_len(p);
+    write_items_seq<P>(out, p, nb, g, kk, acc, blk, std::make_integer_sequence<int, P::NACC>{});
+    if (SUMS) {
+#pragma unroll
+        for (int k = 0; k < P::NSUM; ++k) {
+            sums[k] += __shfl_xor_sync(0xffffffffu, sums[k], 1);
+            sums[k] += __shfl_xor_sync(0xffffffffu, sums[k], 2);
+        }
+        if (kk == 0) {
+#pragma unroll
+            for (int k = 0; k < P::NSUM; ++k) {
+                const int col = (int)(8 * blk(P::SUM0 + k)) + g;
+                if (col < (int)p) out[col] = sums[k];
+            }
+        }
+    }
+}
+
 // SROWS = rows per ring stage (compile-time, so a stage is one straight-line program with
 // the next k-step's fragment loads issued under the current k-step's DMMAs).  Launched with
 // cluster dimension geo.csize (1 = no cluster).
 // Warps [0, consumers) consume; warp `consumers` is the producer; any further warps (the
 // rest of the producer warpgroup of k_widep_wg) follow the producer's unit sequence without
 // issuing anything, so every collective (barrier.sync 1, barrier.cluster) sees all threads.
-template <int SROWS, int R, bool WG>
+template <int SROWS, int R, bool WG, bool BAL = false>
 __device__ __forceinline__ void widep_body(const TileJob& job, const WideGeom& geo, uint32_t tile_rows, double* sm) {
     // ring x (SROWS x pitch) | kSlack doubles | full[ring] | empty[ring]
     const uint32_t p = geo.p, pitch = geo.pitch, nb = geo.nb, ring = geo.ring, K = geo.csize;
@@ -420,9 +586,44 @@ __device__ __forceinline__ void widep_body(const TileJob& job, const WideGeom& g
         for (uint32_t it = 0; next_unit(u, it); ++it) {
             const UnitInfo ui = unit_info(job, geo, tile_rows, unit_tile(u));
             const uint32_t grp = unit_group(u);
+            if constexpr (BAL) {
+            const uint32_t item = __ldg(geo.items + grp * consumers + warp);
+            const uint32_t I = (item >> 11) & 0xfff, J = item & 0x7ff, kind = (item >> 24) & 7;
+            const bool sums = item & kSumsBit;
+            auto wait = [&](uint32_t s, uint32_t phase) { mbar_wait(&full[s], phase); };
+            auto release = [&](uint32_t s) {
+                __syncwarp();
+                if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[s], lane);
+            };
+            // warp-uniform dispatch to the item's straight-line program; an idle (padding) warp of
+            // the last group keeps the ring protocol only
+            if (item & kIdle) {
+                const uint32_t n_stages = (ui.rows + SROWS - 1) / SROWS;
+                for (uint32_t sidx = 0; sidx < n_stages; ++sidx) {
+                    wait(slot, ph);
+                    release(slot);
+                    if (++slot == ring) slot = 0, ph ^= 1;
+                }
+            } else if (kind == kRect) {
+                if (sums) run_item<SROWS, R, Prog<R, kRect>, true>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                else run_item<SROWS, R, Prog<R, kRect>, false>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+            } else if constexpr (BAL && R == 4) {  // the balanced decomposition's kinds (make_items_balanced8)
+                if (kind == kRectCol3) {
+                    if (sums) run_item<SROWS, R, Prog<R, kRectCol3>, true>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                    else run_item<SROWS, R, Prog<R, kRectCol3>, false>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                } else if (kind == kRectRow3) {
+                    run_item<SROWS, R, Prog<R, kRectRow3>, false>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                } else if (kind == kDiagCol) {
+                    if (sums) run_item<SROWS, R, Prog<R, kDiagCol>, true>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                    else run_item<SROWS, R, Prog<R, kDiagCol>, false>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                } else {
+                    run_item<SROWS, R, Prog<R, kDiagRow>, false>(job, geo, ui, I, J, g, kk, sm, slot_elems, slot, ph, wait, release);
+                }
+            }
+            } else {
             const uint32_t item = __ldg(geo.items + grp * consumers + warp);
             const bool idle = item & kIdle;
-            const uint32_t I = (item >> 14) & 0x3fff, J = item & 0x3fff;
+            const uint32_t I = (item >> 11) & 0xfff, J = item & 0x7ff;
             // fragment a reads column colI + 8a (a < R, rectangle I) or colJ + 8(a-R) (rectangle
             // J); columns past p read the zero pad with c = 0, rows past the tile end read c
             const int colI = (int)(8 * R * I) + g, colJ = (int)(8 * R * J) + g;
@@ -449,9 +650,9 @@ __device__ __forceinline__ void widep_body(const TileJob& job, const WideGeom& g
                     if ((uint32_t)lane < K) mbar_arrive_cluster(&empty[slot], lane);
                 };
                 if (sums_here)
-                    consume_stage<SROWS, R, true>(acc, sums, st, pitch, colI, colJ, cw, release);
+                    consume_stage_rect<SROWS, R, true>(acc, sums, st, pitch, colI, colJ, cw, release);
                 else if (!idle)
-                    consume_stage<SROWS, R, false>(acc, sums, st, pitch, colI, colJ, cw, release);
+                    consume_stage_rect<SROWS, R, false>(acc, sums, st, pitch, colI, colJ, cw, release);
                 else
                     release();
                 if (++slot == ring) slot = 0, ph ^= 1;
@@ -480,6 +681,7 @@ __device__ __forceinline__ void widep_body(const TileJob& job, const WideGeom& g
                         if (colJ + 8 * a < (int)p) out[colJ + 8 * a] = sums[a];
                 }
             }
+            }
         }
     }
     // no CTA leaves while a peer may still multicast into it or arrive on its barriers
@@ -503,15 +705,61 @@ __global__ void __launch_bounds__(512, 1) k_widep_wg(TileJob job, WideGeom geo, 
     extern __shared__ __align__(128) double sm[];
     widep_body<SROWS, R, true>(job, geo, tile_rows, sm);
 }
+// k_widep_wg with the item kinds of the balanced decomposition (make_items_balanced8; R = 4).
+// A kernel of its own: compiling the extra programs into k_widep_wg cost its plain-rectangle
+// plans 1-5 % (p = 256 / 512 / 1024).
+template <int SROWS>
+__global__ void __launch_bounds__(512, 1) k_widep_wgb(TileJob job, WideGeom geo, uint32_t tile_rows) {
+    extern __shared__ __align__(128) double sm[];
+    widep_body<SROWS, 4, true, true>(job, geo, tile_rows, sm);
+}
 
 // Rectangles (I <= J) of the nr x nr rectangle grid, dealt to n_groups groups of
 // `consumers` warps (the last groups padded with idle warps).
 std::vector<uint32_t> make_items(uint32_t nr, uint32_t consumers, uint32_t n_groups) {
     std::vector<uint32_t> items;
     for (uint32_t I = 0; I < nr; ++I)
-        for (uint32_t J = I; J < nr; ++J) items.push_back((I << 14) | J);
+        for (uint32_t J = I; J < nr; ++J) items.push_back(item_word(kRect, I, J, I == 0));
     while (items.size() < (size_t)n_groups * consumers) items.push_back(kIdle);
     return items;
+}
+
+// The balanced decomposition for 8 x 8 groups of 4 blocks (p = 249..256, C5's width) in three
+// 12-warp groups: the plain plan gives every SM sub-partition three 16-DMMA rectangles (48 DMMA
+// per k-step) although only 528 of the 576 blocks are upper-triangle blocks (44 per
+// sub-partition).  Here the 8 diagonal groups take their 10 upper blocks plus one 4-block strip
+// each (14 DMMA), cut from the rectangles (I, I+1) (column strips, leaving 4 x 3 rectangles)
+// and (5, 7) (a row strip, leaving a 3 x 4): 20 rectangles of 16, 8 trimmed ones of 12 and 8
+// diagonal items of 14, dealt {16, 16, 12} to 8 sub-partitions and {16, 14, 14} to 4 — 44 DMMA
+// per k-step on every sub-partition, no mirrored block, every column summed once.
+std::vector<uint32_t> make_items_balanced8() {
+    const uint32_t nr = 8, R = 4;
+    std::vector<uint32_t> t16, t12, d14;
+    auto split = [](uint32_t I, uint32_t J) { return J == I + 1 || (I == 5 && J == 7); };
+    for (uint32_t I = 0; I < nr; ++I)
+        for (uint32_t J = I + 1; J < nr; ++J)
+            if (!split(I, J)) t16.push_back(item_word(kRect, I, J, I == 0));
+    for (uint32_t I = 0; I + 1 < nr; ++I) {
+        t12.push_back(item_word(kRectCol3, I, I + 1, I == 0));            // blocks 4(I+1) .. 4(I+1)+2
+        d14.push_back(item_word(kDiagCol, I, R * (I + 1) + R - 1, I == 0));  // + column block 4(I+1)+3
+    }
+    t12.push_back(item_word(kRectRow3, 5, 7, false));            // rows 20..22 x group 7
+    d14.push_back(item_word(kDiagRow, 7, R * 5 + R - 1, false));  // group 7 + row block 23
+    // the items that add column sums first, so they land on distinct sub-partitions
+    std::stable_partition(t16.begin(), t16.end(), [](uint32_t w) { return (w & kSumsBit) != 0; });
+    std::vector<std::vector<uint32_t>> sub(12);  // sub-partition k: group k / 4, warps k % 4 + 4m
+    for (uint32_t k = 0; k < 12; ++k) sub[k].push_back(t16[k]);
+    for (uint32_t k = 0; k < 8; ++k) sub[k].push_back(t16[12 + k]);
+    // t12[0] (sums) away from the sub-partitions holding a summing rectangle (0..5)
+    for (uint32_t k = 0; k < 8; ++k) sub[k].push_back(t12[(k + 2) % 8]);
+    for (uint32_t k = 8; k < 12; ++k) {
+        sub[k].push_back(d14[2 * (k - 8)]);
+        sub[k].push_back(d14[2 * (k - 8) + 1]);
+    }
+    std::vector<uint32_t> tab(3 * 12, kIdle);
+    for (uint32_t k = 0; k < 12; ++k)
+        for (uint32_t m = 0; m < 3; ++m) tab[(k / 4) * 12 + m * 4 + k % 4] = sub[k][m];
+    return tab;
 }
 
 uint32_t env_u32(const char* name, uint32_t dflt) {
@@ -524,6 +772,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 struct Plan {
     int device = -1;
     bool wg = false;  // k_widep_wg (12 consumer warps) instead of k_widep
+    bool bal = false;  // k_widep_wgb: the balanced decomposition (8 x 8 groups of 4 blocks)
     uint32_t p = 0, srows = 0, R = 0, grid_cap = 0;  // grid_cap = clusters in flight
     size_t smem = 0;
     WideGeom geo{};
@@ -538,9 +787,20 @@ struct Plan {
 std::mutex g_plan_mu;
 std::vector<Plan> g_plans;
 
+bool balanced_applies(bool wg, uint32_t R, uint32_t nr) {
+    return wg && R == 4 && nr == 8 && !env_u32("SSTAT_WIDEP_NOBALANCE", 0);
+}
+template <int SROWS, int R>
+void (*kernel_of(bool wg, bool bal))(TileJob, WideGeom, uint32_t) {
+    if constexpr (R == 4)
+        if (bal) return k_widep_wgb<SROWS>;
+    return wg ? k_widep_wg<SROWS, R> : k_widep<SROWS, R>;
+}
+
 template <int SROWS, int R>
 cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster, bool wg) {
-    auto kern = wg ? k_widep_wg<SROWS, R> : k_widep<SROWS, R>;
+    const bool bal = balanced_applies(wg, R, geo.nr);
+    auto kern = kernel_of<SROWS, R>(wg, bal);
     if (wg) geo.consumers = kWgConsumers;
     const int threads = wg ? 512 : (int)(geo.consumers + 1) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -627,6 +887,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster,
     const uint32_t best_clusters = (uint32_t)pick->clusters;
 
     std::vector<uint32_t> tab = make_items(best.nr, best.consumers, best.n_groups);
+    if (bal && best.n_groups == 3) tab = make_items_balanced8();
     uint32_t* d_items = nullptr;
     e = cudaMalloc(&d_items, tab.size() * sizeof(uint32_t));
     if (e != cudaSuccess) return e;
@@ -635,6 +896,7 @@ cudaError_t make_plan(int device, WideGeom geo, Plan& out, bool force_nocluster,
     best.items = d_items;
     out.device = device;
     out.wg = wg;
+    out.bal = bal;
     out.p = geo.p;
     out.srows = SROWS;
     out.R = R;
@@ -666,11 +928,11 @@ cudaError_t launch_plan(const TileJob& job, const Plan& pl, cudaStream_t stream)
     cfg.numAttrs = 1;
     const uint64_t units = tiles * pl.geo.cpt;
     cfg.gridDim = dim3((unsigned)(std::min<uint64_t>(units, pl.grid_cap) * pl.geo.csize));
-    cudaError_t e = cudaLaunchKernelEx(&cfg, pl.wg ? k_widep_wg<SROWS, R> : k_widep<SROWS, R>, job, pl.geo,
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_of<SROWS, R>(pl.wg, pl.bal), job, pl.geo,
                                        widep_tile_rows(pl.geo.p));
     if (e != cudaSuccess) return e;
     if (job.launched && pl.geo.role == 0)  // the clustered launch (the spare one is its helper)
-        *job.launched = pl.wg ? (const void*)k_widep_wg<SROWS, R> : (const void*)k_widep<SROWS, R>;
+        *job.launched = (const void*)kernel_of<SROWS, R>(pl.wg, pl.bal);
     return cudaGetLastError();
 }
 
