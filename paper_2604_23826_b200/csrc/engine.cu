@@ -1392,6 +1392,9 @@ void group_each(sstat_cuda_ctx* g, std::vector<Fail>& fails, std::vector<char>& 
         } catch (const Fail& f) {
             fails[i] = f;
             failed[i] = 1;
+        } catch (const std::bad_alloc&) {
+            fails[i] = Fail{SSTAT_ERR_OOM, "host allocation failed"};
+            failed[i] = 1;
         } catch (const std::exception& e) {
             fails[i] = Fail{SSTAT_ERR_INVALID, e.what()};
             failed[i] = 1;

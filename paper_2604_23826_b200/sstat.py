@@ -382,11 +382,13 @@ class Engine:
             if st != N.OK:
                 raise DeviceError(st, f"sstat_cuda_init_devices failed: {N.status_string(st)}")
             self.devices = devs
+            self._group = True
         else:
             st = self._lib.sstat_cuda_init(ctypes.byref(self._ctx), -1 if device is None else int(device))
             if st != N.OK:
                 raise DeviceError(st, f"sstat_cuda_init failed: {N.status_string(st)}")
             self.devices = [device]
+            self._group = False
         self.rank, self.world = 0, 1
         self._stream_explicit = False  # set_stream called: never re-bind
         self._stream_bound = None  # the torch stream handle the context currently launches on
@@ -420,7 +422,7 @@ class Engine:
         self._stream_bound = cuda_stream
 
     def _follow_torch_stream(self, tensor) -> None:
-        if self._stream_explicit or self.n_devices > 1:
+        if self._stream_explicit or self._group:
             return  # group members keep their own (blocking) streams
         import torch
 
