@@ -1012,7 +1012,7 @@ cudaError_t build_plan(int device, uint32_t p, uint32_t srows, bool wg, Plan& pl
     const uint32_t items = geo.nr * (geo.nr + 1) / 2;
     geo.consumers = std::min<uint32_t>(12, std::max<uint32_t>(1, env_u32("SSTAT_WIDEP_CONSUMERS", items <= 300 ? 4 : 8)));
     // 12-consumer-warp CTAs: registers cap them at 8-row stages for 4x4 rectangles
-    if (wg && geo.R == 4 && srows > 8) srows = 8;
+    if (wg && geo.R == 4 && srows > 8 && !getenv("SSTAT_WIDEP_SROWS")) srows = 8;
     cudaError_t e = make_plan_any(device, geo, srows, pl, false, wg);
     if (e != cudaSuccess) return e;
     const uint64_t slots = (uint64_t)sms_of(device) * pl.resident;
