@@ -153,9 +153,11 @@ int sstat_cuda_init(sstat_cuda_ctx** ctx, int device);
  * ranges are sharded contiguously exactly as in the multi-process path (sstat_shard_ranges),
  * every member accumulates its share in parallel on its own host thread, and the rank buffers
  * meet on devices[0] for the same ascending fold — results are bit-identical to one device and
- * to n_gpus processes.  Exchange: NCCL communicators from ncclCommInitAll when the devices are
- * distinct; peer copies (cudaMemcpyPeerAsync) when a device is listed twice or
- * SSTAT_PEER_EXCHANGE=1.  Group calls:
+ * to n_gpus processes.  Exchange: fused by default — when every member reaches devices[0]'s memory
+ * (the same device, or peer access over NVLink) each member's fold kernel writes its range
+ * partials straight into devices[0]'s gather buffer; otherwise NCCL communicators from
+ * ncclCommInitAll (distinct devices) or peer copies.  SSTAT_GROUP_EXCHANGE=fused|copy|nccl
+ * overrides.  Group calls:
  *   sstat_cuda_dataset / _comoments / _column_sum: a FILE or HOST source is read by every member
  *     (each its own ranges); a DEVICE source is an ARRAY of n_gpus sources, element i = member
  *     i's shard on devices[i] (first_row / n_rows as in the multi-process call);

@@ -233,7 +233,9 @@ struct sstat_cuda_ctx {
     // owns no device state.  Exchange: NCCL (ncclCommInitAll over distinct devices) or peer
     // copies into member 0 (`peer`: a device listed twice, or SSTAT_PEER_EXCHANGE=1).
     std::vector<sstat_cuda_ctx*> members;
-    bool peer = false;
+    bool peer = false;   // exchange by peer copies into member 0
+    bool fused = false;  // exchange fused into the local phase: members write member 0's gather buffer
+    double* ext_rank = nullptr;  // (member of a fused group, during a call) its slot of member 0's gather buffer
     std::unique_ptr<FillPool> gpool;  // one host thread per member for the local phase
     bool is_group() const { return !members.empty(); }
 };
@@ -658,6 +660,7 @@ struct Local {
     bool scanned = false;    // the non-finite scan already ran for this rank
     double* rank_buf = nullptr;
     uint64_t rank_stride = 0;  // kHdr + lmax * E doubles
+    bool ext = false;          // rank_buf is a slot of a group's gather buffer (not this context's d_rank)
 };
 
 void classify(const Plan& P, Local& st) {
@@ -744,23 +747,34 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
     for (uint64_t i = 0; i < L; ++i) fold_k = std::max(fold_k, fold_chunks(tiles_of(P.counts[P.r0 + i])));
 
     const uint64_t rank_stride = kHdr + P.lmax * E;
-    CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
     CUDA_TRY(c->d_flags.reserve(std::max<uint64_t>(L, 1) * 4));
     st.rank_stride = rank_stride;
-    st.rank_buf = c->d_rank.as<double>();
     // the header ([0] lowest failing range, [1] first non-finite index: all-ones = none;
     // [2] the rank's status, [3] spare: 0) and the range flags are only written when something
     // is flagged or failed: reset them only after such a call or a realloc
-    if (!(c->flags_clean && c->clean_rank == c->d_rank.gen && c->clean_flags == c->d_flags.gen && L <= c->clean_len)) {
-        CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, 2 * 8, s));
-        CUDA_TRY(cudaMemsetAsync(c->d_rank.as<double>() + 2, 0, (kHdr - 2) * 8, s));
+    if (c->ext_rank) {
+        // a member of a fused device group: K3a and the scan write this member's slot of member
+        // 0's gather buffer directly (peer stores / atomics over NVLink): the exchange is the fold
+        st.rank_buf = c->ext_rank;
+        st.ext = true;
+        CUDA_TRY(cudaMemsetAsync(st.rank_buf, 0xff, 2 * 8, s));
+        CUDA_TRY(cudaMemsetAsync(st.rank_buf + 2, 0, (kHdr - 2) * 8, s));
         CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
-        c->clean_rank = c->d_rank.gen;
-        c->clean_flags = c->d_flags.gen;
-        c->clean_len = std::max<uint64_t>(L, 1);
+    } else {
+        CUDA_TRY(c->d_rank.reserve(rank_stride * 8));
+        st.rank_buf = c->d_rank.as<double>();
+        if (!(c->flags_clean && c->clean_rank == c->d_rank.gen && c->clean_flags == c->d_flags.gen &&
+              L <= c->clean_len)) {
+            CUDA_TRY(cudaMemsetAsync(c->d_rank.p, 0xff, 2 * 8, s));
+            CUDA_TRY(cudaMemsetAsync(c->d_rank.as<double>() + 2, 0, (kHdr - 2) * 8, s));
+            CUDA_TRY(cudaMemsetAsync(c->d_flags.p, 0, std::max<uint64_t>(L, 1) * 4, s));
+            c->clean_rank = c->d_rank.gen;
+            c->clean_flags = c->d_flags.gen;
+            c->clean_len = std::max<uint64_t>(L, 1);
+        }
     }
     c->flags_clean = false;  // until this call ends with nothing flagged
-    double* rank_buf = c->d_rank.as<double>();
+    double* rank_buf = st.rank_buf;
     uint32_t* d_flags = c->d_flags.as<uint32_t>();
     if (!refexact) {
         CUDA_TRY(c->d_tiles.reserve(std::max<uint64_t>(nt, 1) * E * 8));
@@ -1041,8 +1055,13 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
 void publish_status(sstat_cuda_ctx* c, const Plan& P, Local& st, int status) {
     const uint64_t E = partial_len(P.p), lmax = (P.R + c->world - 1) / c->world;
     st.rank_stride = kHdr + lmax * E;
-    CUDA_TRY(c->d_rank.reserve(st.rank_stride * 8));
-    st.rank_buf = c->d_rank.as<double>();
+    if (c->ext_rank) {
+        st.rank_buf = c->ext_rank;
+        st.ext = true;
+    } else {
+        CUDA_TRY(c->d_rank.reserve(st.rank_stride * 8));
+        st.rank_buf = c->d_rank.as<double>();
+    }
     st.graphable = false;
     const uint64_t hdr[kHdr] = {kNone, kNone, (uint64_t)status, 0};
     CUDA_TRY(cudaMemcpyAsync(st.rank_buf, hdr, sizeof hdr, cudaMemcpyHostToDevice, c->stream));
@@ -1157,7 +1176,7 @@ void run_fold(sstat_cuda_ctx* c, const sstat_cuda_source* src, const Plan& P, co
             out.failed_status = (int)status;
         }
     }
-    c->flags_clean = !any_flag;
+    if (!st.ext) c->flags_clean = !any_flag;  // (a fused group's fold reads the gather buffer)
     if (result_host) std::memcpy(result_host, hres, E * 8);
     if (tm) kernel_name(c->last_kernel, tm->kernel, sizeof tm->kernel);
     if (tm && st.graphable) {  // the graph records three events: K1, then both folds together
@@ -1436,8 +1455,9 @@ int group_publish(sstat_cuda_ctx* g, const std::vector<Fail>& fails, const std::
 }
 
 // Moves every member's rank buffer (stride_doubles each, at bufs[i]) into member 0's gather
-// buffer in rank order: grouped ncclAllGather over the ncclCommInitAll communicators, or peer
-// copies (cudaMemcpyPeerAsync over NVLink) ordered after each member's stream.  Returns member
+// buffer in rank order: grouped ncclAllGather over the ncclCommInitAll communicators, or (no
+// communicators: peer-copy and fused groups — column_sum is not fused) peer copies
+// (cudaMemcpyPeerAsync over NVLink) ordered after each member's stream.  Returns member
 // 0's gathered buffer; member 0's stream is ordered after every contribution.
 void* group_gather(sstat_cuda_ctx* g, const std::vector<const void*>& bufs, uint64_t stride_doubles) {
     const int G = (int)g->members.size();
@@ -1446,7 +1466,7 @@ void* group_gather(sstat_cuda_ctx* g, const std::vector<const void*>& bufs, uint
     std::vector<std::unique_lock<std::mutex>> locks;
     for (sstat_cuda_ctx* m : g->members) locks.emplace_back(m->mu);
     const uint64_t bytes = stride_doubles * 8;
-    if (g->peer) {
+    if (!m0->comm) {  // peer copies (the peer-copy groups, and the calls a fused group does not fuse)
         CUDA_TRY(cudaSetDevice(m0->device));
         CUDA_TRY(m0->d_gather.reserve(bytes * G));
         for (int i = 0; i < G; ++i) {
@@ -1512,16 +1532,49 @@ void run_group(sstat_cuda_ctx* g, const sstat_cuda_source* src, const Plan& P0, 
     std::vector<Fail> fails;
     std::vector<char> failed;
     for (size_t i = 0; i < G; ++i) classify(Ps[i], sts[i]);
+    sstat_cuda_ctx* m0 = g->members[0];
+    const bool fused = g->fused && G > 1;
+    if (fused) {
+        // every member's rank buffer is its slot of member 0's gather buffer (the layout of the
+        // exchange, a function of the plan alone): K3a's stores are the all-gather
+        const uint64_t E = partial_len(P0.p), lmax = (P0.R + G - 1) / G, stride = kHdr + lmax * E;
+        {
+            std::lock_guard<std::mutex> lk(m0->mu);
+            CUDA_TRY(cudaSetDevice(m0->device));
+            CUDA_TRY(m0->d_gather.reserve(G * stride * 8));
+        }
+        for (size_t i = 0; i < G; ++i) g->members[i]->ext_rank = m0->d_gather.as<double>() + i * stride;
+    }
+    struct ClearExt {  // members return to their own rank buffers whatever happens
+        sstat_cuda_ctx* g;
+        ~ClearExt() {
+            for (auto* m : g->members) m->ext_rank = nullptr;
+        }
+    } clear_ext{g};
     group_each(g, fails, failed, [&](size_t i, sstat_cuda_ctx* m) {
         run_local(m, member_src(src, i), Ps[i], files[i], sts[i], tm ? &tms[i] : nullptr);
     });
     const int first_failed = group_publish(g, fails, failed, [&](size_t i, sstat_cuda_ctx* m, int status) {
         publish_status(m, Ps[i], sts[i], status);
     });
-    std::vector<const void*> bufs(G);
-    for (size_t i = 0; i < G; ++i) bufs[i] = sts[i].rank_buf;
-    const double* fold_buf = static_cast<const double*>(group_gather(g, bufs, sts[0].rank_stride));
-    sstat_cuda_ctx* m0 = g->members[0];
+    const double* fold_buf;
+    if (fused) {  // member 0's stream waits for every member's local phase
+        std::lock_guard<std::mutex> lk0(m0->mu);
+        for (size_t i = 1; i < G; ++i) {
+            sstat_cuda_ctx* m = g->members[i];
+            std::lock_guard<std::mutex> lk(m->mu);
+            CUDA_TRY(cudaSetDevice(m->device));
+            CUDA_TRY(cudaEventRecord(m->ev[5], m->stream));
+            CUDA_TRY(cudaSetDevice(m0->device));
+            CUDA_TRY(cudaStreamWaitEvent(m0->stream, m->ev[5], 0));
+        }
+        CUDA_TRY(cudaSetDevice(m0->device));
+        fold_buf = m0->d_gather.as<double>();
+    } else {
+        std::vector<const void*> bufs(G);
+        for (size_t i = 0; i < G; ++i) bufs[i] = sts[i].rank_buf;
+        fold_buf = static_cast<const double*>(group_gather(g, bufs, sts[0].rank_stride));
+    }
     std::lock_guard<std::mutex> lk(m0->mu);
     sstat_cuda_timings t0{};
     run_fold(m0, member_src(src, 0), Ps[0], sts[0], fold_buf, (int)G, result_host, out, tm ? &t0 : nullptr);
@@ -1751,9 +1804,32 @@ int sstat_cuda_init_devices(sstat_cuda_ctx** out, int n_gpus, const int* devices
         // the members share the host: feeder threads split between them
         m->host_threads = std::max(1u, default_host_threads() / (unsigned)n_gpus);
     }
-    const char* force_peer = getenv("SSTAT_PEER_EXCHANGE");
-    g->peer = n_gpus > 1 && (!distinct || (force_peer && atoi(force_peer) != 0));
-    if (st == SSTAT_OK && n_gpus > 1 && !g->peer) {
+    // Exchange: fused (every member reaches member 0's memory: the same device, or peer access
+    // over NVLink) unless SSTAT_GROUP_EXCHANGE picks "copy" (peer copies) or "nccl"
+    // (ncclCommInitAll + grouped all-gather; also the default when a member cannot reach member 0)
+    bool reach = true;
+    for (int i = 1; i < n_gpus && st == SSTAT_OK; ++i) {
+        if (devices[i] == devices[0]) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, devices[i], devices[0]);
+        if (can) {
+            cudaSetDevice(devices[i]);
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(devices[0], 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) can = 0;
+            cudaGetLastError();
+        }
+        reach = reach && can;
+    }
+    const char* xenv = getenv("SSTAT_GROUP_EXCHANGE");
+    const std::string xmode = xenv ? xenv : "";
+    if (n_gpus > 1) {
+        if (xmode == "copy") g->peer = true;
+        else if (xmode == "nccl") g->peer = !distinct;  // NCCL needs distinct devices
+        else if (reach) g->fused = true;
+        else g->peer = !distinct;
+        if (getenv("SSTAT_PEER_EXCHANGE") && atoi(getenv("SSTAT_PEER_EXCHANGE")) != 0) g->peer = true, g->fused = false;
+    }
+    if (st == SSTAT_OK && n_gpus > 1 && !g->peer && !g->fused) {
         std::vector<ncclComm_t> comms(n_gpus);
         if (ncclCommInitAll(comms.data(), n_gpus, devices) != ncclSuccess) st = SSTAT_ERR_NCCL;
         else
@@ -1767,6 +1843,7 @@ int sstat_cuda_init_devices(sstat_cuda_ctx** out, int n_gpus, const int* devices
             cudaDeviceEnablePeerAccess(devices[0], 0);
             cudaGetLastError();  // already enabled / no P2P: cudaMemcpyPeerAsync still works
         }
+    if (st == SSTAT_OK && g->fused && getenv("SSTAT_DEBUG")) fprintf(stderr, "sstat: device group of %d, fused exchange\n", n_gpus);
     if (st != SSTAT_OK) {
         for (auto* m : g->members) {
             free_device_state(m);

@@ -81,13 +81,17 @@ def test_group_of_one_is_the_device_context(engine, tmp_path):
     g.close()
 
 
+@pytest.mark.parametrize("mode", ["fused", "copy"])
 @pytest.mark.parametrize("W", [2, 3, 5, 8])
-def test_group_peer_exchange_bit_identical(engine, tmp_path, W):
-    """W members on one GPU: per-member shards, peer-copy gather, device K3b over W rank
-    buffers — the single-device bits (fast mode, reference order, Binary32Diagnostic), and
-    the same for host / file sources every member streams its own ranges from."""
+def test_group_exchange_bit_identical(engine, tmp_path, W, mode, monkeypatch):
+    """W members on one GPU: per-member shards, the exchange (fused: every member's K3a and scan
+    write its slot of member 0's gather buffer directly; copy: member buffers copied into it), the
+    device K3b over W rank buffers — the single-device bits (fast mode, reference order,
+    Binary32Diagnostic), and the same for host / file sources every member streams its own
+    ranges from."""
     from paper_2604_23826_b200 import Engine
 
+    monkeypatch.setenv("SSTAT_GROUP_EXCHANGE", mode)
     n, p, chunk = 300_007, 16, 4099
     D = gen(engine, n, p)
     pl = plan(n, chunk)
@@ -132,11 +136,14 @@ def test_group_wide_p_bit_identical(engine, p):
     g.close()
 
 
-def test_group_nonfinite_reports_lowest_range(engine):
+@pytest.mark.parametrize("mode", ["fused", "copy"])
+def test_group_nonfinite_reports_lowest_range(engine, mode, monkeypatch):
     """Non-finite values on two members: every member scans before the exchange, the rank
     headers meet in member 0, and the error is the single-device one (lowest failing range,
     its first non-finite row / column, reduce.hpp:111-134)."""
     from paper_2604_23826_b200 import Engine, ReductionError
+
+    monkeypatch.setenv("SSTAT_GROUP_EXCHANGE", mode)
 
     torch = torch_mod()
     n, p, chunk = 100_000, 16, 1000
@@ -160,13 +167,16 @@ def test_group_nonfinite_reports_lowest_range(engine):
     g.close()
 
 
-def test_group_member_failure_is_published(engine):
+@pytest.mark.parametrize("mode", ["fused", "copy"])
+def test_group_member_failure_is_published(engine, mode, monkeypatch):
     """A member whose local phase fails (its shard does not cover its ranges) publishes its
     status in its rank header; the exchange and fold still run, the rank headers name that
     member (the group checks them against the host-side failures), and the call raises the
     member's own error — the path a failing rank of a multi-process run takes instead of
     leaving its peers in the collective.  The next call succeeds."""
     from paper_2604_23826_b200 import Engine
+
+    monkeypatch.setenv("SSTAT_GROUP_EXCHANGE", mode)
 
     n, p, chunk = 90_000, 16, 3000
     D = gen(engine, n, p)
@@ -319,3 +329,26 @@ def test_small_plans_match_the_reference(engine, oracle, n, chunk):
         engine.dataset_suffstats(D, schema(p), pl)
     assert e.value.cause.row() == n // 3 and e.value.cause.column() == 7
     assert e.value.range_index() == (n // 3) // chunk
+
+
+def test_group_member0_state_after_fused_calls(engine):
+    """The fused exchange leaves member 0's own rank buffer alone: a chunk with a non-finite value
+    accumulated through the group, then a fused dataset pass, then a clean chunk — each call
+    reports exactly its own outcome (no stale error header)."""
+    import torch
+
+    from paper_2604_23826_b200 import Chunk, Engine, NonFiniteError
+
+    g = Engine(devices=[0, 0])
+    p = 8
+    bad = torch.ones((100, p), dtype=torch.float64, device="cuda")
+    bad[40, 3] = float("inf")
+    with pytest.raises(NonFiniteError):
+        g.accumulate_chunk(Chunk(0, 100, p, bad), schema(p))
+    n = 50_000
+    D = gen(engine, n, p, kind=2)
+    pl = plan(n, 5_000)
+    assert g.dataset_suffstats(shards(D, pl, 2), schema(p), pl).bit_equal(engine.dataset_suffstats(D, schema(p), pl))
+    good = torch.ones((100, p), dtype=torch.float64, device="cuda")
+    assert g.accumulate_chunk(Chunk(0, 100, p, good), schema(p)).n == 100
+    g.close()
