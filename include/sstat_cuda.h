@@ -256,7 +256,7 @@ int sstat_cuda_comoments(sstat_cuda_ctx* ctx, const sstat_cuda_source* src, uint
  * runs after the all-gather: rank q's buffer starts at buf + q*rank_stride with a
  * 4-double header ({lowest failing range, first non-finite row*p+col, status, 0}), then its ranges [floor(qR/W), floor((q+1)R/W)) of p + p(p+1)/2
  * doubles each.  flags & SSTAT_FLAG_REFEXACT (or Binary32Diagnostic): the reference's
- * ascending fold from +0.0; otherwise the 8-lane fast fold of the default mode.
+ * ascending fold from +0.0; otherwise the 32-lane fast fold of the default mode.
  * out receives p + p(p+1)/2 doubles. */
 int sstat_fold_ranges_host(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
                            uint32_t precision, uint32_t flags, double* out);

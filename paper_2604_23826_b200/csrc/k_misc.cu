@@ -71,10 +71,11 @@ __global__ void k_final_fold_seq(const double* __restrict__ buf, uint64_t rank_s
     out[e] = fold_entry(buf, rank_stride, n_ranges, world, p, precision, e);
 }
 
-// K3b, fast mode (fold_fast): blocks of 256 threads over 32-entry slices.
-__global__ void __launch_bounds__(256) k_final_fold_fast(const double* __restrict__ buf, uint64_t rank_stride,
-                                                         uint64_t n_ranges, int world, uint32_t p, double* out) {
-    __shared__ double sm[256];
+// K3b, fast mode (fold_fast): blocks of kFoldLanes x 32 threads over 32-entry slices.
+constexpr int kFoldBlock = kFoldLanes * 32;
+__global__ void __launch_bounds__(kFoldBlock) k_final_fold_fast(const double* __restrict__ buf, uint64_t rank_stride,
+                                                                uint64_t n_ranges, int world, uint32_t p, double* out) {
+    __shared__ double sm[kFoldBlock];
     const uint64_t E = partial_len(p);
     const int le = threadIdx.x & 31, q = threadIdx.x >> 5;
     if (blockIdx.x == 0)  // append the rank headers
@@ -82,14 +83,15 @@ __global__ void __launch_bounds__(256) k_final_fold_fast(const double* __restric
             out[E + h] = buf[(h / kHdr) * rank_stride + h % kHdr];
     const uint64_t e = blockIdx.x * 32ull + le;
     double s = 0.0;
-    if (e < E) {  // fold_lane's order, four loads in flight ahead of the adds
+    if (e < E) {  // fold_lane's order, eight loads in flight ahead of the adds
+        constexpr int U = 8;
         uint64_t r = q;
-        for (; r + 3 * kFoldLanes < n_ranges; r += 4 * kFoldLanes) {
-            double v[4];
+        for (; r + (U - 1) * kFoldLanes < n_ranges; r += U * kFoldLanes) {
+            double v[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldcg(range_partial(buf, rank_stride, n_ranges, world, E, r + u * kFoldLanes) + e);
+            for (int u = 0; u < U; ++u) v[u] = __ldcg(range_partial(buf, rank_stride, n_ranges, world, E, r + u * kFoldLanes) + e);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) s += v[u];
+            for (int u = 0; u < U; ++u) s += v[u];
         }
         for (; r < n_ranges; r += kFoldLanes) s += __ldcg(range_partial(buf, rank_stride, n_ranges, world, E, r) + e);
     }
@@ -426,7 +428,7 @@ cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t 
         k_final_fold_seq<<<(unsigned)((E + 127) / 128), 128, 0, stream>>>(buf, rank_stride, n_ranges, world, p, precision,
                                                                            out);
     else
-        k_final_fold_fast<<<(unsigned)((E + 31) / 32), 256, 0, stream>>>(buf, rank_stride, n_ranges, world, p, out);
+        k_final_fold_fast<<<(unsigned)((E + 31) / 32), kFoldBlock, 0, stream>>>(buf, rank_stride, n_ranges, world, p, out);
     return cudaGetLastError();
 }
 

@@ -47,7 +47,7 @@ cudaError_t launch_find_nonfinite(const double* base, uint64_t base_row, const u
 
 // K3b: fold over all n_ranges global ranges.  reference_order: ascending from +0.0
 // (reduce.hpp:142-145, fold_entry; precision 1 rounds every add through binary32 like
-// merge_suffstats, suffstats.cpp:92-98); otherwise the 8-lane fast fold (fold_fast).
+// merge_suffstats, suffstats.cpp:92-98); otherwise the 32-lane fast fold (fold_fast).
 // Range r lives in rank q = owner(r) at buf + q*rank_stride + kHdr + (r - first(q))*E.
 cudaError_t launch_final_fold(const double* buf, uint64_t rank_stride, uint64_t n_ranges, int world, uint32_t p,
                               uint32_t precision, bool reference_order, double* out, cudaStream_t stream);

@@ -713,7 +713,7 @@ def fold_range_partials(partials: np.ndarray, schema: DatasetSchema, plan: Reduc
                         flags: int = 0) -> SuffStats:
     """The dataset result from all R ranges' partials (R x E, range order) — e.g. checkpointed
     pieces from range_partials — folded on the host in the device's own order (fast mode: the
-    8-lane fold; SSTAT_FLAG_REFEXACT / Binary32Diagnostic: the reference's ascending fold), so it
+    32-lane fold; SSTAT_FLAG_REFEXACT / Binary32Diagnostic: the reference's ascending fold), so it
     is bit-identical to dataset_suffstats over the same plan."""
     schema.validate()
     p = schema.column_count()

@@ -164,15 +164,15 @@ def test_host_fold_equals_reference_fold_for_any_world(oracle, W):
 
 
 @pytest.mark.parametrize("W", [1, 2, 3, 8])
-def test_host_fast_fold_is_the_8_lane_order(oracle, W):
-    """The default-mode fold: lane q sums ranges q, q+8, ... from +0.0, then lanes 0..7 in order —
-    the same bits for any rank layout."""
+def test_host_fast_fold_is_the_32_lane_order(oracle, W):
+    """The default-mode fold: lane q sums ranges q, q+32, ... from +0.0, then lanes 0..31 in
+    order — the same bits for any rank layout."""
     from paper_2604_23826_b200 import _native as N
     from paper_2604_23826_b200 import shard_ranges
 
     lib = N.load()
     rng = np.random.default_rng(W)
-    p, R = 5, 37
+    p, R = 5, 137
     E = p + p * (p + 1) // 2
     parts = rng.normal(size=(R, E)) * 10.0 ** rng.integers(-8, 8, size=(R, E))
     per_rank = [parts[shard_ranges(R, q, W)[0]:shard_ranges(R, q, W)[1]] for q in range(W)]
@@ -183,9 +183,9 @@ def test_host_fast_fold_is_the_8_lane_order(oracle, W):
     want = np.zeros(E)
     for e in range(E):
         t = 0.0
-        for q in range(8):
+        for q in range(32):
             s = 0.0
-            for r in range(q, R, 8):
+            for r in range(q, R, 32):
                 s += parts[r, e]
             t += s
         want[e] = t
