@@ -352,3 +352,39 @@ def test_group_member0_state_after_fused_calls(engine):
     good = torch.ones((100, p), dtype=torch.float64, device="cuda")
     assert g.accumulate_chunk(Chunk(0, 100, p, good), schema(p)).n == 100
     g.close()
+
+
+def test_group_reader_and_pieces(engine, tmp_path):
+    """A device group reading a RowReader (both members call it, each for its own ranges) and a
+    file in reference order through slots smaller than a range (pieces per member): the
+    single-device bits."""
+    from paper_2604_23826_b200 import Engine, RowReader
+
+    n, p, chunk = 200_003, 40, 1 << 15
+    D = gen(engine, n, p, kind=2, seed=12)
+    pl = plan(n, chunk)
+    H = D.cpu().numpy()
+    calls = []
+
+    def read(row, k, scratch):
+        calls.append(row)
+        ctypes.memmove(scratch, H[row:row + k].ctypes.data, k * p * 8)
+        return scratch
+
+    path = tmp_path / "gp.bin"
+    hdr = bytearray(64)
+    hdr[0:8] = b"SSTATBIN"
+    hdr[8:12] = (1).to_bytes(4, "little")
+    hdr[12:20] = n.to_bytes(8, "little")
+    hdr[20:24] = p.to_bytes(4, "little")
+    with open(path, "wb") as f:
+        f.write(hdr)
+        H.tofile(f)
+    g = Engine(devices=[0, 0, 0])
+    g.set_staging(2, 1 << 20)
+    for flags in (0, 2):
+        want = engine.dataset_suffstats(D, schema(p), pl, flags=flags)
+        assert g.dataset_suffstats(RowReader(read, n), schema(p), pl, flags=flags).bit_equal(want), flags
+        assert g.dataset_suffstats(str(path), schema(p), pl, flags=flags).bit_equal(want), flags
+    assert min(calls) == 0 and max(calls) > n // 2  # every member read its own ranges
+    g.close()
