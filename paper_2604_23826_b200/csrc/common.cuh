@@ -75,7 +75,9 @@ __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p);
 __device__ __forceinline__ double2 ld_stream2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
 
 // Per-rank header in front of the range partials: [0] lowest failing global range
-// (UINT64_MAX = none), [1] first non-finite linear index row*p + col.
+// (UINT64_MAX = none), [1] first non-finite linear index row*p + col (UINT64_MAX = none),
+// [2] the rank's status (0 = ok; a failed rank's sstat_status, so its peers fail with it
+// instead of waiting in the exchange), [3] spare (0).
 constexpr uint32_t kHdr = 4;
 
 // Where range r's partial sits in the gathered rank buffers: rank q = owner(r) with

@@ -5,9 +5,10 @@
 // dataset_suffstats):  the std::thread pool pulling ranges becomes HBM-resident (or
 // streamed) row shards accumulated tile by tile by K1/K2, the per-range partial slots
 // become a device buffer of per-range partials (K3a), and the ascending range fold
-// becomes K3b — run after an NCCL all-gather when rows are sharded over GPUs.
-// Results are a fixed function of (data, plan): bit-identical for any GPU count,
-// grid size or staging layout.
+// becomes K3b — run after the exchange when rows are sharded over GPUs: an NCCL all-gather
+// between processes (one per GPU), or, for a device group driven by one process, K3a writing
+// each member's partials straight into member 0's gather buffer.  Results are a fixed
+// function of (data, plan): bit-identical for any GPU count, grid size or staging layout.
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
