@@ -222,8 +222,8 @@ int main() {
     std::printf("DMMA occupancy: %2d warps/SM, %2d chains/warp: %.2f TFLOP/s\n", wpb * bpsm, nacc, 2 * fma / ms / 1e9);
   };
   for (int w : {1, 2, 4, 8}) run_occ(dmma_peak<16>, 16, w, 1);
-  for (int w : {4, 8, 16}) run_occ(dmma_outer, 16, w, 1);
-  for (int w : {4, 8, 16}) run_occ(dmma_outer_lds, 16, w, 1);
+  for (int w : {4, 8, 12, 16}) run_occ(dmma_outer, 16, w, 1);
+  for (int w : {4, 8, 12, 16}) run_occ(dmma_outer_lds, 16, w, 1);
   run_occ(dmma_peak<16>, 16, 4, 2);
   run_occ(dmma_peak<16>, 16, 4, 4);
   run_dmma(dmma_peak<1>, 1, 4);
