@@ -899,7 +899,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
         CUDA_TRY(cudaGraphLaunch(c->graph, s));
         if (tm) {
             tm->bytes_read += (P.span_end - P.span_begin) * p * 8;
-            tm->kernel_launches += shift ? 4 : 3;
+            tm->kernel_launches += (shift && !small ? 1 : 0) + 2 + (one_range ? 0 : 1);  // [gather] K1 K3a [K3b]
         }
         return;  // everything up to the read-back is in the graph
     }
