@@ -325,6 +325,7 @@ def run_ours(args):
         return pl, r0, r1 - r0
 
     eng = Engine(local)
+    eng.collect_timings = True  # K1's CUDA-event time for the roofline; the kernel name
     if world > 1:
         obj = [Engine.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)

@@ -171,7 +171,7 @@ inline SuffStats dataset_suffstats(Engine& eng, const std::filesystem::path& dat
     sstat_cuda_error err{};
     const int st = sstat_cuda_dataset(eng.get(), &src, p, starts.data(), counts.data(), starts.size(),
                                       static_cast<std::uint32_t>(plan.precision), flags, &n, sums.data(), cross.data(),
-                                      &t, &err);
+                                      timings ? &t : nullptr, &err);
     if (st != SSTAT_OK) detail::rethrow(st, err, true);
     fill_timings(timings, t);
     return detail::make_result(schema, plan.precision, n, sums, cross);
@@ -201,7 +201,7 @@ inline SuffStats dataset_suffstats(Engine& eng, const double* rows, std::uint64_
     sstat_cuda_error err{};
     const int st = sstat_cuda_dataset(eng.get(), &src, p, starts.data(), counts.data(), starts.size(),
                                       static_cast<std::uint32_t>(plan.precision), flags, &n, sums.data(), cross.data(),
-                                      &t, &err);
+                                      timings ? &t : nullptr, &err);
     if (st != SSTAT_OK) detail::rethrow(st, err, true);
     fill_timings(timings, t);
     return detail::make_result(schema, plan.precision, n, sums, cross);

@@ -106,7 +106,11 @@ def test_wide_p256_multi_range_multi_tile_vs_reference(engine, reference):
     pl = ReductionPlan(plan_partitions(n, chunk))
     assert len(pl.partition.ranges) == 10  # 9 x 2^18 rows (8 K2 tiles each) + a 140800-row tail
     sc = DatasetSchema.generic(p, False)
-    fast = engine.dataset_suffstats(D, sc, pl)
+    engine.collect_timings = True
+    try:
+        fast = engine.dataset_suffstats(D, sc, pl)
+    finally:
+        engine.collect_timings = False
     kernel = engine.last_timings.kernel.decode()
     assert kernel.startswith("k_widep"), kernel
     H = D.cpu().numpy()

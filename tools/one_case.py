@@ -11,6 +11,7 @@ from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_par
 p, n = int(sys.argv[1]), int(float(sys.argv[2]))
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 eng = Engine(0)
+eng.collect_timings = True
 D = torch.empty((n, p), dtype=torch.float64, device="cuda")
 eng.generate(D, 2, 1, 1.0, 0, 0, n, p)
 plan = ReductionPlan(plan_partitions(n, 1 << 20))

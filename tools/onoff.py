@@ -1,5 +1,5 @@
-"""C2 step with and without the library's timing events, alternated to cancel clock drift:
-    python tools/onoff.py [ROUNDS] [K]"""
+"""C2 (or C1) step with and without the library's timing events, alternated to cancel clock drift:
+    python tools/onoff.py [ROUNDS] [K] [c1]"""
 import os
 import sys
 
@@ -10,14 +10,15 @@ from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_par
 
 ROUNDS = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 50
-n, p = 100_000_000, 16
+C1 = len(sys.argv) > 3 and sys.argv[3] == "c1"
+n, p, kind, n_int = (1_000_000, 9, 1, 0) if C1 else (100_000_000, 16, 0, 2)
 eng = Engine(0)
 s = torch.cuda.current_stream()
 eng.set_stream(s.cuda_stream)
 D = torch.empty((n, p), dtype=torch.float64, device="cuda")
-eng.generate(D, 0, 42, 1.0, 2, 0, n, p)
+eng.generate(D, kind, 42, 1.0, n_int, 0, n, p)
 plan = ReductionPlan(plan_partitions(n, 1 << 20))
-sc = DatasetSchema.generic(p, False)
+sc = DatasetSchema.generic(p, C1)
 acc = {True: [], False: []}
 for r in range(ROUNDS):
     for timed in ((True, False) if r % 2 == 0 else (False, True)):

@@ -13,6 +13,7 @@ from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_par
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 8e9
 eng = Engine(0)
+eng.collect_timings = True
 for p in [int(x) for x in os.environ.get("SWEEP_P", "8,16,24,32,40,48,56,64,65,72,80,96,104,112,120,128,192,256,384,512").split(",")]:
     n = int(budget // (8 * p))
     D = torch.empty((n, p), dtype=torch.float64, device="cuda")

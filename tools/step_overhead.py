@@ -12,6 +12,7 @@ from paper_2604_23826_b200 import _native as N
 
 n, p = 100_000_000, 16
 eng = Engine(0)
+eng.collect_timings = True
 D = torch.empty((n, p), dtype=torch.float64, device="cuda")
 eng.generate(D, 0, 42, 1.0, 2, 0, n, p)
 plan = ReductionPlan(plan_partitions(n, 1 << 20))

@@ -14,6 +14,7 @@ from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_par
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 100_000_000
 p = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 eng = Engine(0)
+eng.collect_timings = True
 stream = torch.cuda.current_stream()
 eng.set_stream(stream.cuda_stream)
 D = torch.empty((n, p), dtype=torch.float64, device="cuda")

@@ -12,6 +12,7 @@ from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_par
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 4e10
 eng = Engine(0)
+eng.collect_timings = True
 os.environ["SSTAT_SPLITP"] = "0"
 for p in [int(x) for x in os.environ.get("SWEEP_P", "136,192,256,384,512").split(",")]:
     n = int(budget // (8 * p))
