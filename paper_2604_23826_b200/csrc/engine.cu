@@ -211,7 +211,9 @@ struct sstat_cuda_ctx {
     std::vector<DevBuf> slots;
     std::vector<HostBuf> bounce;
     std::vector<cudaEvent_t> ev_copied, ev_free;
-    cudaEvent_t ev[6] = {};
+    // ev[0..4]: K1 / fold / exchange brackets; ev[5], ev[6]: the H2D span of a streamed call
+    cudaEvent_t ev[7] = {};
+    bool h2d_timed = false;  // ev[5] / ev[6] recorded by this call's stream_chunks
     // per-call state kept across calls: the last uploaded plan (skip identical re-uploads)
     // and whether the rank header / range flags are still in their reset state
     std::vector<uint64_t> meta_last;
@@ -493,6 +495,7 @@ void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint
         const uint32_t slot = (uint32_t)(chunk % c->n_slots);
         const uint64_t row0 = unit_row[u], nrows = bytes / row_bytes;
         CUDA_TRY(cudaStreamWaitEvent(c->copy, c->ev_free[slot], 0));
+        if (tm && chunk == 0) CUDA_TRY(cudaEventRecord(c->ev[5], c->copy));
         const void* host_src;
         if (hr.pinned) {
             host_src = hr.host_row(row0);
@@ -518,6 +521,10 @@ void stream_chunks(sstat_cuda_ctx* c, const HostRows& hr, const std::vector<uint
         }
         u = v;
         ++chunk;
+    }
+    if (tm && chunk > 0) {  // h2d_seconds: first copy start to last copy end on the copy stream
+        CUDA_TRY(cudaEventRecord(c->ev[6], c->copy));
+        c->h2d_timed = true;
     }
 }
 
@@ -727,6 +734,7 @@ bool host_pinned(const sstat_cuda_source* src) {
 void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile& file, Local& st,
                sstat_cuda_timings* tm) {
     check_plan(c, src, P, file);
+    c->h2d_timed = false;
     const int world = call_world(c, P);
     const bool comoments = st.comoments, refexact = st.refexact, shift = st.shift;
     // K2 stages at least one k-step (4 rows) of every column in shared memory, double-buffered
@@ -1197,6 +1205,7 @@ void run_fold(sstat_cuda_ctx* c, const sstat_cuda_source* src, const Plan& P, co
         tm->fold_seconds += ms * 1e-3;
         cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
         tm->exchange_seconds += ms * 1e-3;
+        if (c->h2d_timed && cudaEventElapsedTime(&ms, c->ev[5], c->ev[6]) == cudaSuccess) tm->h2d_seconds += ms * 1e-3;
         tm->n_local_ranges = (uint32_t)L;
     }
 }
