@@ -102,7 +102,7 @@ typedef struct {
 
 /* ReductionTimings (reduce.hpp:56-60), device-side breakdown. */
 typedef struct {
-    double h2d_seconds;      /* host->device copy busy time (host / file sources)   */
+    double h2d_seconds;      /* host->device copies, first start to last end (host / file sources) */
     double kernel_seconds;   /* accumulate kernels, device events                   */
     double exchange_seconds; /* NCCL all-gather of per-range partials               */
     double fold_seconds;     /* per-range + ascending range folds                   */
