@@ -441,15 +441,18 @@ struct Plan {
     std::vector<uint64_t> tile_row, tile_rows;  // host view of local tiles (streaming)
 };
 
-// K1's tile height for a plan: kTileRows, or — when the whole plan (every rank's ranges) has
-// fewer than kFillTiles such tiles, so the grid would leave CTA slots idle (C1: 245 tiles for
-// 592 slots) — the largest power of two >= kMinTileRows giving at least kFillTiles tiles.
-// A function of the global plan alone: every rank and GPU count cuts the same tiles.
+// K1's tile height for a plan: kBigTileRows when the whole plan (every rank's ranges) has at
+// least kBigTileMin such tiles (C2: 6104) and p > 8 (p <= 8 measured 3 % slower with them);
+// else kTileRows, or — when the plan has fewer than kFillTiles such tiles, so the grid would
+// leave CTA slots idle (C1: 245 tiles for 592 slots) — the largest power of two >=
+// kMinTileRows giving at least kFillTiles tiles.  A function of the global plan alone: every
+// rank and GPU count cuts the same tiles.
 uint64_t smallp_tile_rows(const Plan& P) {
     if (const char* env = getenv("SSTAT_K1_TILE_ROWS")) {  // experiment knob: a fixed height (multiple of 32)
         const uint64_t tr = strtoull(env, nullptr, 10);
-        if (tr >= 32 && tr <= kTileRows && tr % 32 == 0) return tr;
+        if (tr >= 32 && tr <= kBigTileRows && tr % 32 == 0) return tr;
     }
+    if (P.p > 8 && P.total / kBigTileRows >= kBigTileMin) return kBigTileRows;
     if (P.total / kTileRows >= kFillTiles) return kTileRows;  // sum of ceil(count / TR) >= total / TR
     uint64_t TR = kTileRows;
     for (; TR > kMinTileRows; TR /= 2) {
@@ -841,7 +844,7 @@ void run_local(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFile
         // short tiles (smallp_tile_rows): K1 and K3a read each range's shift row in place, so the
         // gather kernel drops out; one_range: K3b (a copy of one partial) drops out too.
         const bool timed = tm != nullptr;
-        const bool small = TR != kTileRows;
+        const bool small = TR < kTileRows;
         const bool one_range = P.R == 1;
         st.hdr_first = one_range;
         const std::vector<uint64_t> key = {

@@ -133,9 +133,10 @@ __device__ int canonical_slot(int e, uint32_t p) {
     return a < (int)p ? a : -1;
 }
 
-// RT = false: tiles of kTileRows rows (a compile-time bound: the loop is fully unrolled and
-// software-pipelined — measured faster); RT = true: job.tile_rows (small plans).
-template <int NB, bool VEC, bool X1 = false, bool RT = false>
+// TRC: the tile height as a compile-time constant — kTileRows (the loop is fully unrolled and
+// software-pipelined, measured faster) or kBigTileRows (large plans) — or 0: job.tile_rows
+// at run time (small plans).
+template <int NB, bool VEC, bool X1 = false, uint32_t TRC = kTileRows>
 __device__ __forceinline__ void smallp_body(const TileJob& job) {
     using C = SmallP<NB, VEC, X1>;
     constexpr int U = C::U;
@@ -148,7 +149,7 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
     for (uint64_t t = job.tile_begin + blockIdx.x; t < job.tile_end; t += gridDim.x) {
         const uint32_t r = range_of_tile(job.tile_prefix, job.n_ranges, t);
         const uint64_t rs = __ldg(job.range_start + r), rc = __ldg(job.range_count + r);
-        const uint32_t TR = RT ? job.tile_rows : kTileRows;
+        const uint32_t TR = TRC ? TRC : job.tile_rows;
         const uint64_t row0 = rs + (t - __ldg(job.tile_prefix + r)) * TR;
         const uint64_t left = rs + rc - row0;
         const uint32_t rows = left < TR ? (uint32_t)left : TR;
@@ -157,7 +158,7 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
         // shift row c of this range (the gathered table; reading it in place from the shard
         // costs this kernel 16 registers and 1.6% of its bandwidth — measured)
         const double* crow = job.shift != nullptr ? job.shift + (uint64_t)r * p
-                             : (RT && job.shift_in_place && rc) ? job.base + (rs - job.base_row) * p
+                             : (!TRC && job.shift_in_place && rc) ? job.base + (rs - job.base_row) * p
                                                                : nullptr;
         double c[NB];
 #pragma unroll
@@ -271,31 +272,31 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
 // overrides): 3 for NB = 3..4 (<= 85 registers, 24 warps; p = 24: 4.2 -> 5.8 TB/s, p = 32:
 // 4.2 -> 5.0), 2 for NB = 5 (<= 128; p = 40: +35 %).  NB = 6 spills under a floor of 2 and
 // loses 14 %; NB >= 6 stay unbounded.
-template <int NB, bool VEC, bool RT>
+template <int NB, bool VEC, uint32_t TRC>
 __global__ void __launch_bounds__(kThreads) k_smallp(TileJob job) {
-    smallp_body<NB, VEC, false, RT>(job);
+    smallp_body<NB, VEC, false, TRC>(job);
 }
-template <int NB, bool VEC, int MINB, bool RT>
+template <int NB, bool VEC, int MINB, uint32_t TRC>
 __global__ void __launch_bounds__(kThreads, MINB) k_smallp_floor(TileJob job) {
-    smallp_body<NB, VEC, false, RT>(job);
+    smallp_body<NB, VEC, false, TRC>(job);
 }
 
-template <int NB, bool RT>
+template <int NB, uint32_t TRC>
 __global__ void __launch_bounds__(kThreads) k_smallp_x1(TileJob job) {
-    smallp_body<NB, false, true, RT>(job);
+    smallp_body<NB, false, true, TRC>(job);
 }
 
-template <int NB, bool RT>
+template <int NB, uint32_t TRC>
 cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, false, true>::FRAG;
-    static std::atomic<int> cached[64];  // per instantiation (NB, RT)
+    static std::atomic<int> cached[64];  // per instantiation (NB, TRC)
     int dev = 0;
     cudaGetDevice(&dev);
     int per_sm = dev < 64 ? cached[dev].load() : 0;
     if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_smallp_x1<NB, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_smallp_x1<NB, TRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp_x1<NB, RT>, kThreads, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_smallp_x1<NB, TRC>, kThreads, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
         if (dev < 64) cached[dev].store(per_sm);
@@ -303,23 +304,23 @@ cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
-    k_smallp_x1<NB, RT><<<(unsigned)grid, kThreads, smem, stream>>>(job);
-    if (job.launched) *job.launched = (const void*)k_smallp_x1<NB, RT>;
+    k_smallp_x1<NB, TRC><<<(unsigned)grid, kThreads, smem, stream>>>(job);
+    if (job.launched) *job.launched = (const void*)k_smallp_x1<NB, TRC>;
     return cudaGetLastError();
 }
 
-template <int NB, bool VEC, bool RT>
+template <int NB, bool VEC, uint32_t TRC>
 cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     constexpr size_t smem = sizeof(double) * kWarps * SmallP<NB, VEC>::FRAG;
     int minb = NB == 3 || NB == 4 ? 3 : (NB == 5 ? 2 : 0);
     if (const char* env = getenv("SSTAT_K1_MINB")) minb = atoi(env);
-    void (*kern)(TileJob) = k_smallp<NB, VEC, RT>;
+    void (*kern)(TileJob) = k_smallp<NB, VEC, TRC>;
     if constexpr (NB >= 3 && NB <= 4) {
-        if (minb == 3) kern = k_smallp_floor<NB, VEC, 3, RT>;
-        else if (minb == 2) kern = k_smallp_floor<NB, VEC, 2, RT>;
+        if (minb == 3) kern = k_smallp_floor<NB, VEC, 3, TRC>;
+        else if (minb == 2) kern = k_smallp_floor<NB, VEC, 2, TRC>;
         else minb = 0;
     } else if constexpr (NB == 5) {
-        if (minb == 2) kern = k_smallp_floor<NB, VEC, 2, RT>;
+        if (minb == 2) kern = k_smallp_floor<NB, VEC, 2, TRC>;
         else minb = 0;
     } else {
         minb = 0;
@@ -346,7 +347,7 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-template <bool RT>
+template <uint32_t TRC>
 cudaError_t launch_smallp_rt(const TileJob& job, int sms, cudaStream_t stream) {
     const uint32_t p = job.p;
     const int nb = (int)((p + 7) / 8);
@@ -357,37 +358,38 @@ cudaError_t launch_smallp_rt(const TileJob& job, int sms, cudaStream_t stream) {
     // +4 / +8 %)
     if (p % 8 == 1 && p > 1 && !getenv("SSTAT_K1_NO_X1")) {
         switch (p / 8) {
-            case 1: return launch_nb_x1<1, RT>(job, sms, stream);
-            case 2: return launch_nb_x1<2, RT>(job, sms, stream);
-            case 3: return launch_nb_x1<3, RT>(job, sms, stream);
+            case 1: return launch_nb_x1<1, TRC>(job, sms, stream);
+            case 2: return launch_nb_x1<2, TRC>(job, sms, stream);
+            case 3: return launch_nb_x1<3, TRC>(job, sms, stream);
             // NB = 4 (p = 33): 136 registers, one CTA per SM — measured 18 % below the
             // occupancy-floored 5-block-row kernel, which it keeps
-            case 5: return launch_nb_x1<5, RT>(job, sms, stream);
-            case 6: return launch_nb_x1<6, RT>(job, sms, stream);
-            case 7: return launch_nb_x1<7, RT>(job, sms, stream);
+            case 5: return launch_nb_x1<5, TRC>(job, sms, stream);
+            case 6: return launch_nb_x1<6, TRC>(job, sms, stream);
+            case 7: return launch_nb_x1<7, TRC>(job, sms, stream);
             default: break;
         }
     }
     switch (nb) {
-        case 1: return launch_nb<1, false, RT>(job, sms, stream);
-        case 2: return vec ? launch_nb<2, true, RT>(job, sms, stream) : launch_nb<2, false, RT>(job, sms, stream);
-        case 3: return launch_nb<3, false, RT>(job, sms, stream);
-        case 4: return vec ? launch_nb<4, true, RT>(job, sms, stream) : launch_nb<4, false, RT>(job, sms, stream);
-        case 5: return launch_nb<5, false, RT>(job, sms, stream);
-        case 6: return vec ? launch_nb<6, true, RT>(job, sms, stream) : launch_nb<6, false, RT>(job, sms, stream);
-        case 7: return launch_nb<7, false, RT>(job, sms, stream);
-        case 8: return vec ? launch_nb<8, true, RT>(job, sms, stream) : launch_nb<8, false, RT>(job, sms, stream);
+        case 1: return launch_nb<1, false, TRC>(job, sms, stream);
+        case 2: return vec ? launch_nb<2, true, TRC>(job, sms, stream) : launch_nb<2, false, TRC>(job, sms, stream);
+        case 3: return launch_nb<3, false, TRC>(job, sms, stream);
+        case 4: return vec ? launch_nb<4, true, TRC>(job, sms, stream) : launch_nb<4, false, TRC>(job, sms, stream);
+        case 5: return launch_nb<5, false, TRC>(job, sms, stream);
+        case 6: return vec ? launch_nb<6, true, TRC>(job, sms, stream) : launch_nb<6, false, TRC>(job, sms, stream);
+        case 7: return launch_nb<7, false, TRC>(job, sms, stream);
+        case 8: return vec ? launch_nb<8, true, TRC>(job, sms, stream) : launch_nb<8, false, TRC>(job, sms, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
 }  // namespace
 
-// Full-height tiles take the kernels with the compile-time tile height; small plans' shorter
-// tiles (job.tile_rows < kTileRows) the runtime-height instances.
+// Full-height tiles (kTileRows, or kBigTileRows for large plans) take the kernels with the
+// compile-time tile height; small plans' shorter tiles the runtime-height instances.
 cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream) {
-    return job.tile_rows == kTileRows ? launch_smallp_rt<false>(job, sms, stream)
-                                      : launch_smallp_rt<true>(job, sms, stream);
+    if (job.tile_rows == kTileRows) return launch_smallp_rt<kTileRows>(job, sms, stream);
+    if (job.tile_rows == kBigTileRows) return launch_smallp_rt<kBigTileRows>(job, sms, stream);
+    return launch_smallp_rt<0>(job, sms, stream);
 }
 
 }  // namespace sstat_b200
