@@ -211,8 +211,9 @@ struct sstat_cuda_ctx {
     std::vector<DevBuf> slots;
     std::vector<HostBuf> bounce;
     std::vector<cudaEvent_t> ev_copied, ev_free;
-    // ev[0..4]: K1 / fold / exchange brackets; ev[5], ev[6]: the H2D span of a streamed call
-    cudaEvent_t ev[7] = {};
+    // ev[0..4]: K1 / fold / exchange brackets; ev[5], ev[6]: the H2D span of a streamed call;
+    // ev[7]: a group member's end of local work, joined by member 0's stream
+    cudaEvent_t ev[8] = {};
     bool h2d_timed = false;  // ev[5] / ev[6] recorded by this call's stream_chunks
     // per-call state kept across calls: the last uploaded plan (skip identical re-uploads)
     // and whether the rank header / range flags are still in their reset state
@@ -1486,9 +1487,9 @@ void* group_gather(sstat_cuda_ctx* g, const std::vector<const void*>& bufs, uint
             sstat_cuda_ctx* m = g->members[i];
             if (i > 0) {
                 CUDA_TRY(cudaSetDevice(m->device));
-                CUDA_TRY(cudaEventRecord(m->ev[5], m->stream));
+                CUDA_TRY(cudaEventRecord(m->ev[7], m->stream));
                 CUDA_TRY(cudaSetDevice(m0->device));
-                CUDA_TRY(cudaStreamWaitEvent(m0->stream, m->ev[5], 0));
+                CUDA_TRY(cudaStreamWaitEvent(m0->stream, m->ev[7], 0));
             }
             CUDA_TRY(cudaMemcpyPeerAsync(m0->d_gather.as<char>() + i * bytes, m0->device, bufs[i], m->device, bytes,
                                          m0->stream));
@@ -1577,9 +1578,9 @@ void run_group(sstat_cuda_ctx* g, const sstat_cuda_source* src, const Plan& P0, 
             sstat_cuda_ctx* m = g->members[i];
             std::lock_guard<std::mutex> lk(m->mu);
             CUDA_TRY(cudaSetDevice(m->device));
-            CUDA_TRY(cudaEventRecord(m->ev[5], m->stream));
+            CUDA_TRY(cudaEventRecord(m->ev[7], m->stream));
             CUDA_TRY(cudaSetDevice(m0->device));
-            CUDA_TRY(cudaStreamWaitEvent(m0->stream, m->ev[5], 0));
+            CUDA_TRY(cudaStreamWaitEvent(m0->stream, m->ev[7], 0));
         }
         CUDA_TRY(cudaSetDevice(m0->device));
         fold_buf = m0->d_gather.as<double>();
@@ -1597,6 +1598,13 @@ void run_group(sstat_cuda_ctx* g, const sstat_cuda_source* src, const Plan& P0, 
         throw fails[first_failed];
     }
     if (tm) {
+        // every member's copy span (member 0's stream has waited for all of them: complete)
+        for (size_t i = 0; i < G; ++i) {
+            sstat_cuda_ctx* m = g->members[i];
+            float ms = 0;
+            if (m->h2d_timed && cudaEventElapsedTime(&ms, m->ev[5], m->ev[6]) == cudaSuccess)
+                tms[i].h2d_seconds = ms * 1e-3;
+        }
         tms[0].fold_seconds += t0.fold_seconds;
         tms[0].exchange_seconds += t0.exchange_seconds;
         tms[0].kernel_launches += t0.kernel_launches;

@@ -59,6 +59,16 @@ def test_big_tiles_bit_identical_across_sources_and_groups(engine, p):
     assert np.array_equal(a.sums[:2], c.sums[:2])  # integer-valued columns: exact either way
     assert cs_err(a.cross, c.cross, p) < 1e-13
     assert np.max(np.abs(a.sums - c.sums) / np.maximum(np.abs(c.sums), 1.0)) < 1e-12
+    if p == 16:  # the co-moments ride on the same K1 tiles: big against 4096-row
+        m_big = engine.comoments(D, sc, plan)
+        os.environ["SSTAT_K1_TILE_ROWS"] = "4096"
+        try:
+            m_4k = engine.comoments(D, sc, plan)
+        finally:
+            del os.environ["SSTAT_K1_TILE_ROWS"]
+        assert m_big.n == m_4k.n == n
+        assert np.max(np.abs(m_big.mean - m_4k.mean) / np.maximum(np.abs(m_4k.mean), 1.0)) < 1e-13
+        assert cs_err(m_big.m2, m_4k.m2, p) < 1e-12
     # host-streamed (pinned, 4-slot ring): the same tiles, the same bits
     H = torch.empty((n, p), dtype=torch.float64, pin_memory=True)
     H.copy_(D)

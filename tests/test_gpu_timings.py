@@ -64,3 +64,14 @@ def test_host_source_timings(engine):
     b = engine.dataset_suffstats(H, sc, plan)
     assert a.bit_equal(b) and a.bit_equal(engine.dataset_suffstats(D, sc, plan))
     assert np.isfinite(a.cross).all()
+    # a device group of two members, each streaming its ranges of the same pinned array: the
+    # longest member copy span
+    from paper_2604_23826_b200 import Engine
+
+    g = Engine(devices=[0, 0])
+    try:
+        tg = ReductionTimings()
+        assert g.dataset_suffstats(H, sc, plan, timings=tg).bit_equal(a)
+        assert tg.read_seconds > 0 and tg.bytes_read == n * p * 8
+    finally:
+        g.close()
