@@ -422,6 +422,16 @@ class Engine:
         self._stream_explicit = True
         self._stream_bound = cuda_stream
 
+    @staticmethod
+    def _wait_producer(tensor) -> None:
+        """A group member launches on its own blocking stream, ordered after the legacy default
+        stream only: a shard produced on another torch stream is waited for on the host first."""
+        import torch
+
+        s = torch.cuda.current_stream(tensor.device)
+        if s.cuda_stream != 0:
+            s.synchronize()
+
     def _follow_torch_stream(self, tensor) -> None:
         if self._stream_explicit or self._group:
             return  # group members keep their own (blocking) streams
@@ -554,6 +564,7 @@ class Engine:
             for i, shard in enumerate(dataset):
                 if not _is_torch_cuda(shard):
                     raise TypeError("device-group shards must be CUDA tensors")
+                self._wait_producer(shard)
                 f, _ = shard_ranges(R, i, len(dataset))
                 _check_width(shard, p)
                 ptr, k = self._rows_pointer(shard, None)
@@ -579,7 +590,9 @@ class Engine:
             _check_width(dataset, p)
             ptr, keep = self._rows_pointer(dataset, None)
             cuda = _is_torch_cuda(dataset)
-            if cuda:
+            if cuda and self._group:
+                self._wait_producer(dataset)
+            elif cuda:
                 self._follow_torch_stream(dataset)
             src.kind = N.SRC_DEVICE if cuda else N.SRC_HOST
             src.ptr = ptr

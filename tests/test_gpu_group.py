@@ -388,3 +388,39 @@ def test_group_reader_and_pieces(engine, tmp_path):
         assert g.dataset_suffstats(str(path), schema(p), pl, flags=flags).bit_equal(want), flags
     assert min(calls) == 0 and max(calls) > n // 2  # every member read its own ranges
     g.close()
+
+
+def test_group_and_explicit_stream_ordering_without_sync(engine):
+    """Shards written by asynchronous torch kernels on a side stream reach a device group (whose
+    members launch on their own streams) only after the producer is done; an engine bound with
+    set_stream to the producer's stream is ordered after it on the device."""
+    from paper_2604_23826_b200 import Engine
+
+    torch = torch_mod()
+    n, p = 4_000_000, 16
+    pl = plan(n, 1 << 20)
+    X = gen(engine, n, p, seed=9)
+    torch.cuda.synchronize()
+    want = engine.dataset_suffstats(X, schema(p), pl)
+    s = torch.cuda.Stream()
+    g = Engine(devices=[0, 0])
+    e = Engine(0)
+    e.set_stream(s.cuda_stream)
+    assert g.n_devices == 2 and e.n_devices == 1
+    try:
+        with torch.cuda.stream(s):
+            D = torch.zeros((n, p), dtype=torch.float64, device="cuda")
+            for _ in range(3):
+                D.copy_(X)
+                D.mul_(1.0)
+            parts = shards(D, pl, 2)
+            got_g = g.dataset_suffstats(parts, schema(p), pl)
+        assert got_g.bit_equal(want)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                D.mul_(1.0)
+            got_e = e.dataset_suffstats(D, schema(p), pl)
+        assert got_e.bit_equal(want)
+    finally:
+        g.close()
+        e.close()
