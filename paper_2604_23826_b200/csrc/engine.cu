@@ -571,7 +571,8 @@ void check_plan(sstat_cuda_ctx* c, const sstat_cuda_source* src, Plan& P, BinFil
             throw f;
         }
     } else if (src->kind == SSTAT_SRC_DEVICE || src->kind == SSTAT_SRC_HOST || src->kind == SSTAT_SRC_READER) {
-        if (src->kind == SSTAT_SRC_READER ? !src->read_rows : (!src->ptr && P.total > 0)) {
+        // (a rank or group member without ranges may pass an empty source: no rows, no pointer)
+        if (src->kind == SSTAT_SRC_READER ? !src->read_rows : (!src->ptr && src->n_rows > 0)) {
             inv.msg = src->kind == SSTAT_SRC_READER ? "null read_rows callback" : "null row pointer";
             throw inv;
         }
