@@ -3,8 +3,9 @@ from a few rows to a few million, chunk sizes from a handful of rows to the whol
 short ranges, ranges shorter than a tile, one range), integer-valued and Gaussian columns with
 small and large means.  Per case:
   * the fast pass from HBM equals, bit for bit, the same pass from pinned and pageable host
-    memory, from an SSTATBIN file and from a two-member device group (one fixed function of the
-    rows and the plan, whatever the source or GPU count);
+    memory, from an SSTATBIN file (with the default and a random staging ring and feeder thread
+    count) and from a two-member device group (one fixed function of the rows and the plan,
+    whatever the source, staging or GPU count);
   * it agrees with the oracle's reference-order reduction (reduce.hpp:70-146 restated,
     oracle/sstat_oracle.c) to the Cauchy-Schwarz-normalised 1e-12 bar, integer-valued columns
     exactly;
@@ -74,6 +75,16 @@ def test_fuzz_sources_groups_and_oracle(engine, oracle, tmp_path, seed):
     path = str(tmp_path / "x.bin")
     sstatbin(path, H)
     assert engine.dataset_suffstats(path, sc, plan).bit_equal(got), what + " file"
+    # a second engine with a random staging ring (slots grow to the largest unit when smaller)
+    rng = np.random.default_rng(seed)
+    e2 = Engine(0)
+    try:
+        e2.set_staging(int(rng.integers(2, 6)), int(rng.integers(1 << 20, 64 << 20)))  # >= 1 MiB
+        e2.set_host_threads(int(rng.integers(1, 9)))
+        for src in (P, H, path):
+            assert e2.dataset_suffstats(src, sc, plan).bit_equal(got), what + " staging"
+    finally:
+        e2.close()
     R = len(plan.partition.ranges)
     g = Engine(devices=[0, 0])
     try:
