@@ -173,3 +173,52 @@ def test_fuzz_nonfinite_error(engine, oracle, tmp_path, seed):
     finally:
         g.close()
     os.remove(path)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_chunks_readers_and_binary32(engine, oracle, seed):
+    """accumulate_chunk on host and device chunks at random start rows (reference order: the
+    oracle's bits; fast: within the bars), a RowReader source equal to the array source, and
+    Binary32Diagnostic (the reference's float accumulation) bit-identical to the oracle."""
+    import ctypes
+
+    import torch
+
+    from paper_2604_23826_b200 import (Chunk, DatasetSchema, PrecisionMode, ReductionPlan, RowReader,
+                                       plan_partitions)
+
+    rng, p, n, chunk, n_int, mu = case(200 + seed)
+    H = oracle.generate(0, 1200 + seed, mu, n_int, 0, n, p)
+    D = torch.from_numpy(H).cuda()
+    sc = DatasetSchema.generic(p, False)
+    what = f"p={p} n={n} chunk={chunk}"
+    start = int(rng.integers(0, 1 << 40))
+    want = oracle.accumulate_chunk(H, p, start)
+    for vals in (H, D):
+        exact = engine.accumulate_chunk(Chunk(start, n, p, vals), sc, flags=REFEXACT)
+        assert exact.n == n and np.array_equal(bits(exact.cross), bits(want[2])), what
+        assert np.array_equal(bits(exact.sums), bits(want[1])), what
+        fast = engine.accumulate_chunk(Chunk(start, n, p, vals), sc)
+        assert cs_err(fast.cross, want[2], p) <= 1e-12, what
+
+    plan = ReductionPlan(plan_partitions(n, chunk))
+    Hp = torch.from_numpy(H).pin_memory()
+
+    def point(row, k, scratch):
+        return Hp.data_ptr() + row * p * 8
+
+    def fill(row, k, scratch):
+        ctypes.memmove(scratch, H[row:row + k].ctypes.data, k * p * 8)
+        return scratch
+
+    base = engine.dataset_suffstats(D, sc, plan)
+    for fn in (point, fill):
+        assert engine.dataset_suffstats(RowReader(fn, n), sc, plan).bit_equal(base), (what, fn.__name__)
+
+    starts, counts = oracle.plan_partitions(n, chunk)
+    want32 = oracle.run_reduction(H, p, starts, counts, workers=4, precision=1)
+    plan32 = ReductionPlan(plan_partitions(n, chunk), 1, PrecisionMode(1))
+    for src in (D, H):
+        got32 = engine.dataset_suffstats(src, sc, plan32)
+        assert np.array_equal(bits(got32.sums), bits(want32[1])), what
+        assert np.array_equal(bits(got32.cross), bits(want32[2])), what
