@@ -1,1 +1,1 @@
-for t in . ab/nowait ab/nowaitdexp_norelease; do echo "== $t"; SWEEP_P=256 timeout 300 python ab/p_sweep_tree.py $t 1e11; done > gpurun_out/k2_exp.log 2>&1
+for t in . ab/nowait ab/nowaitdexp_norelease; do echo "== $t"; SWEEP_P=256 timeout 300 python tools/ab/p_sweep_tree.py $t 1e11; done > gpurun_out/k2_exp.log 2>&1
