@@ -135,7 +135,9 @@ typedef struct {
     uint32_t reserved;
     const void* ptr;      /* DEVICE/HOST: rows [first_row, first_row + n_rows)       */
     uint64_t first_row;   /* absolute dataset row held at ptr[0] (READER: first row  */
-    uint64_t n_rows;      /* rows addressable (READER: rows read_rows can serve)     */
+    uint64_t n_rows;      /* rows addressable (READER: rows read_rows can serve);    */
+                          /* 0 with ptr NULL: an empty shard (a rank or group member */
+                          /* holding no ranges)                                      */
     const char* path;     /* FILE                                                    */
     sstat_read_rows_fn read_rows; /* READER                                          */
     void* user;           /* READER: passed to read_rows                             */
