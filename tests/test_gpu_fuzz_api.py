@@ -222,3 +222,38 @@ def test_fuzz_chunks_readers_and_binary32(engine, oracle, seed):
         got32 = engine.dataset_suffstats(src, sc, plan32)
         assert np.array_equal(bits(got32.sums), bits(want32[1])), what
         assert np.array_equal(bits(got32.cross), bits(want32[2])), what
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_groups_every_call(engine, seed):
+    """Device groups of 1-6 members (more members than ranges included) on random plans: every
+    call — dataset in both modes, co-moments, column_sum, range_partials — gives the single-device
+    bits, from per-member CUDA shards and from one shared host array."""
+    import torch
+
+    from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_partitions
+
+    rng, p, n, chunk, n_int, mu = case(400 + seed)
+    W = int(rng.integers(1, 7))
+    D = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    engine.generate(D, 0, 500 + seed, mu, n_int, 0, n, p)
+    torch.cuda.synchronize()
+    H = D.cpu().numpy()
+    plan = ReductionPlan(plan_partitions(n, chunk))
+    sc = DatasetSchema.generic(p, False)
+    R = len(plan.partition.ranges)
+    what = f"W={W} p={p} n={n} R={R}"
+    g = Engine(devices=[0] * W)
+    try:
+        parts = group_parts(D, plan, W)
+        for flags in (0, REFEXACT):
+            want = engine.dataset_suffstats(D, sc, plan, flags=flags)
+            assert g.dataset_suffstats(parts, sc, plan, flags=flags).bit_equal(want), (what, flags)
+            assert g.dataset_suffstats(H, sc, plan, flags=flags).bit_equal(want), (what, flags, "host")
+        a, b = engine.comoments(D, sc, plan), g.comoments(parts, sc, plan)
+        assert np.array_equal(bits(a.m2), bits(b.m2)) and np.array_equal(bits(a.mean), bits(b.mean)), what
+        col = int(rng.integers(0, p))
+        ca, cb = engine.column_sum(D, col, plan, p=p), g.column_sum(parts, col, plan, p=p)
+        assert bits(ca.float_sum) == bits(cb.float_sum) and ca.exact_sum == cb.exact_sum, what
+    finally:
+        g.close()
