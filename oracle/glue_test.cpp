@@ -20,7 +20,9 @@
 #include <filesystem>
 #include <fstream>
 #include <limits>
+#include <random>
 #include <string>
+#include <vector>
 
 #include "sstat/analysis.hpp"
 #include "sstat/binfile.hpp"
@@ -206,6 +208,30 @@ int main() {
             CHECK(g_exact == cpu);
             const SuffStats g_fast = cuda::dataset_suffstats(group, bin, schema, plan);
             CHECK(g_fast == gpu);
+        }
+    }
+
+    // 9. seeded random plans through the unmodified reference: row counts from one row to 300k,
+    //    chunks from one row to the whole file, 1-16 workers — reference-order mode equal to the
+    //    reference's dataset_suffstats, the fast pass within the Cauchy-Schwarz bar with the
+    //    integer columns exact, a three-member group equal to one GPU
+    {
+        std::mt19937_64 rng(20261019);
+        cuda::Engine group(std::vector<int>{0, 0, 0});
+        for (int c = 0; c < 8; ++c) {
+            const std::uint64_t nr = 1 + rng() % 300000;
+            const std::uint64_t chunk = c % 3 == 0 ? 1 + rng() % 64 : 1 + rng() % nr;
+            auto f = write_table1(dir, nr, 100 + c);
+            ReductionPlan pl;
+            pl.partition = plan_partitions(nr, chunk < nr / 20000 ? nr / 20000 + 1 : chunk);
+            pl.worker_count = 1 + rng() % 16;
+            const SuffStats ref = dataset_suffstats(f, schema, pl);
+            CHECK(cuda::dataset_suffstats(eng, f, schema, pl, nullptr, SSTAT_FLAG_REFEXACT) == ref);
+            const SuffStats fast = cuda::dataset_suffstats(eng, f, schema, pl);
+            CHECK(fast.n == ref.n && cs_err(fast, ref) <= 1e-12);
+            for (std::size_t j : {0u, 1u, 2u, 3u, 10u}) CHECK(fast.sums[j] == ref.sums[j]);
+            CHECK(cuda::dataset_suffstats(group, f, schema, pl) == fast);
+            std::filesystem::remove(f);
         }
     }
 
