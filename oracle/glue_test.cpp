@@ -231,6 +231,26 @@ int main() {
             CHECK(fast.n == ref.n && cs_err(fast, ref) <= 1e-12);
             for (std::size_t j : {0u, 1u, 2u, 3u, 10u}) CHECK(fast.sums[j] == ref.sums[j]);
             CHECK(cuda::dataset_suffstats(group, f, schema, pl) == fast);
+            // column_sum (reference order: the reference's float sum; exact sums either way) and
+            // the co-moments on the same plan
+            for (std::size_t col : {std::size_t(0), std::size_t(9)}) {
+                const auto cs_ref = column_sum(f, col, pl);
+                const auto cs_ex = cuda::column_sum(eng, f, col, pl, SSTAT_FLAG_REFEXACT);
+                const auto cs_fast = cuda::column_sum(eng, f, col, pl);
+                CHECK(cs_ex.float_sum == cs_ref.float_sum && cs_ex.exact_sum == cs_ref.exact_sum);
+                CHECK(cs_fast.exact_sum == cs_ref.exact_sum && cs_fast.exact_note == cs_ref.exact_note);
+            }
+            auto per = [&](const Chunk& ch) { return accumulate_comoments(ch, schema); };
+            auto mrg = [](CoMoments a, CoMoments b) { return merge_comoments(std::move(a), b); };
+            const CoMoments cm_ref = run_reduction(f, pl, per, mrg, CoMoments::empty(schema));
+            const CoMoments cm_gpu = cuda::dataset_comoments(eng, f, schema, pl);
+            CHECK(cm_gpu.n == cm_ref.n);
+            if (nr > 1)
+                for (std::size_t j = 0; j < 11; ++j)
+                    for (std::size_t k = j; k < 11; ++k) {
+                        const double sc = std::sqrt(cm_ref.m2.at(j, j) * cm_ref.m2.at(k, k));
+                        if (sc > 0) CHECK(std::fabs(cm_gpu.m2.at(j, k) - cm_ref.m2.at(j, k)) <= 1e-12 * sc);
+                    }
             std::filesystem::remove(f);
         }
     }
