@@ -34,6 +34,9 @@ Beside it, on the same run (each its own JSON object in the line):
                  on the SAME C2 bytes (N = 1), all host threads, plus the parity of our result
                  against it (parity_c2_vs_reference)
   next_rows      column_sum and co-moments on the resident C2 shard (N = 1)
+  c1             C1, the reference's CPU-runnable case (1e6 x (8 + ID), one range, N = 1): the
+                 call time through the API and the accumulate kernel's, L2 flushed (a 256 MB read)
+                 before every call
 
 --impl reference runs only the CPU reference arm (rank 0) on the C2 bytes and prints its line.
 """
@@ -404,6 +407,47 @@ def run_ours(args):
                           "gb_per_s": local_rows * p * 8 / t_cm / 1e9},
         }
 
+    # ---------------- C1: 1e6 x (8 + ID), one range (the reference's CPU-runnable case) ----------------
+    c1_line = None
+    if not args.no_c1 and world == 1:
+        n1, p1 = 1_000_000, 9
+        D1 = torch.empty((n1, p1), dtype=torch.float64, device="cuda")
+        eng.generate(D1, 1, SEED, MU, 0, 0, n1, p1)
+        plan1 = ReductionPlan(plan_partitions(n1, CHUNK_ROWS))
+        sc1 = DatasetSchema.generic(p1, True)
+        # L2 flush by a 256 MB read (> the 126 MB L2) before every call: clean lines, so the call
+        # neither finds its rows in L2 nor pays for another buffer's write-backs
+        flush = torch.ones(32 << 20, dtype=torch.float64, device="cuda")
+        k1s, calls, calls_timed = [], [], []
+        for timed in (False, True):
+            eng.collect_timings = timed
+            for it in range(205):
+                flush.sum()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                eng.dataset_suffstats(D1, sc1, plan1)
+                b.record(stream)
+                torch.cuda.synchronize()
+                if it >= 5:
+                    (calls_timed if timed else calls).append(a.elapsed_time(b) * 1e3)
+                    if timed:
+                        k1s.append(eng.last_timings.kernel_seconds * 1e6)
+        eng.collect_timings = True
+        med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
+        k1_us = med(k1s)
+        hbm_peak, _ = peaks()
+        c1_line = {"rows": n1, "p": p1, "ranges": 1, "value": n1 / (med(calls) * 1e-6), "unit": "rows/s",
+                   "call_us": med(calls), "call_us_with_timings": med(calls_timed), "k1_us": k1_us,
+                   "k1_gb_per_s": n1 * p1 * 8 / (k1_us * 1e-6) / 1e9,
+                   "k1_frac": n1 * p1 * 8 / (k1_us * 1e-6) / 1e9 / hbm_peak,
+                   "kernel": eng.last_timings.kernel.decode(), "calls": len(calls),
+                   "l2": "flushed before every call (a 256 MB read)",
+                   "what": "dataset_suffstats(CUDA tensor) of 1e6 rows x (8 + ID): K1 on 512-row tiles, K3a, "
+                           "read-back, one replayed graph; call_us = device time from before the call to after "
+                           "its return (medians over 200 calls)"}
+        del D1, flush
+        torch.cuda.empty_cache()
+
     # ---------------- e2e: the public API from pinned host memory ----------------
     e2e, cpu, parity, H = None, None, None, None
     shard_bytes = local_rows * p * 8
@@ -597,6 +641,7 @@ def run_ours(args):
             "resident_c4": c4,
             "c5": c5,
             "next_rows": next_rows,
+            "c1": c1_line,
         }
         print(json.dumps(line), flush=True)
     eng.close()
@@ -744,6 +789,7 @@ def main():
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 call-time leg")
     ap.add_argument("--dry-run", action="store_true", help="launcher + rank layout only, CPU (gloo)")
     args = ap.parse_args()
     world_env = os.environ.get("WORLD_SIZE")
