@@ -11,13 +11,14 @@ namespace sstat_b200 {
 // any grid size, GPU count or staging layout.  K1's tiles are kTileRows = 4096 rows
 // (8 warps x 128 k-steps); large plans (at least kBigTileMin tiles of kBigTileRows, p > 8)
 // take kBigTileRows = 16384 (a quarter of the per-tile epilogues and partials: C2's K1
-// +3 %, profiles/r02_k1_tile_height_ab.log); plans too small to fill the GPU with kTileRows:
-// smallp_tile_rows (engine.cu) then halves the height, down to kMinTileRows, until the
-// whole plan has kFillTiles tiles — a function of the plan alone, the same on every rank.
+// +3 %, profiles/r02_k1_tile_height_ab.log); plans too small to fill the GPU with kTileRows
+// take the shortest height whose tiles fit one wave of K1's CTA slots (smallp_tile_rows,
+// engine.cu) — a function of the plan alone, the same on every rank.
 constexpr uint32_t kTileRows = 4096;
 constexpr uint32_t kBigTileRows = 16384;
 constexpr uint32_t kMinTileRows = 256;
 constexpr uint64_t kFillTiles = 2ull * 148 * 4;   // twice K1's resident CTA slots on a B200
+constexpr uint64_t kWaveTiles = 148ull * 4;       // K1's resident CTA slots on a B200
 constexpr uint64_t kBigTileMin = 8ull * 148 * 4;  // eight waves of big tiles
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;

@@ -444,10 +444,12 @@ struct Plan {
 
 // K1's tile height for a plan: kBigTileRows when the whole plan (every rank's ranges) has at
 // least kBigTileMin such tiles (C2: 6104) and p > 8 (p <= 8 measured 3 % slower with them);
-// else kTileRows, or — when the plan has fewer than kFillTiles such tiles, so the grid would
-// leave CTA slots idle (C1: 245 tiles for 592 slots) — the largest power of two >=
-// kMinTileRows giving at least kFillTiles tiles.  A function of the global plan alone: every
-// rank and GPU count cuts the same tiles.
+// kTileRows when it has at least kFillTiles of those; else — a plan too small to fill the GPU
+// with 4096-row tiles (C1: 245 tiles for 592 CTA slots) — the shortest height (a multiple of 32,
+// at least kMinTileRows) whose tiles fit one wave of K1's CTA slots (C1: 1696 rows, 590 tiles).
+// One wave measured best with L2 flushed before every call (C1 57.5 -> 48.8 us per call, 2e6 x 16
+// 82 -> 73 us; the previous rule, powers of two down to at least two waves, gave C1 512-row
+// tiles).  A function of the global plan alone: every rank and GPU count cuts the same tiles.
 uint64_t smallp_tile_rows(const Plan& P) {
     if (const char* env = getenv("SSTAT_K1_TILE_ROWS")) {  // experiment knob: a fixed height (multiple of 32)
         const uint64_t tr = strtoull(env, nullptr, 10);
@@ -455,13 +457,22 @@ uint64_t smallp_tile_rows(const Plan& P) {
     }
     if (P.p > 8 && P.total / kBigTileRows >= kBigTileMin) return kBigTileRows;
     if (P.total / kTileRows >= kFillTiles) return kTileRows;  // sum of ceil(count / TR) >= total / TR
-    uint64_t TR = kTileRows;
-    for (; TR > kMinTileRows; TR /= 2) {
-        uint64_t tiles = 0;
-        for (uint64_t i = 0; i < P.R && tiles < kFillTiles; ++i) tiles += (P.counts[i] + TR - 1) / TR;
-        if (tiles >= kFillTiles) break;
+    if (P.R > kWaveTiles) return kTileRows;  // a tile per range at least: one wave is out of reach
+    auto tiles_of = [&](uint64_t tr) {
+        uint64_t t = 0;
+        for (uint64_t i = 0; i < P.R; ++i) t += (P.counts[i] + tr - 1) / tr;
+        return t;
+    };
+    // tiles_of falls as the height grows: the smallest multiple of 32 in [lo, kTileRows] that fits
+    uint64_t lo = std::max<uint64_t>(kMinTileRows, ((P.total + kWaveTiles - 1) / kWaveTiles + 31) / 32 * 32);
+    if (lo >= kTileRows || tiles_of(kTileRows) > kWaveTiles) return kTileRows;
+    uint64_t hi = kTileRows;  // fits
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2 / 32 * 32;
+        if (tiles_of(mid) <= kWaveTiles) hi = mid;
+        else lo = mid + 32;
     }
-    return TR;
+    return hi;
 }
 
 uint64_t tile_rows_for(const Plan& P) { return P.p > 64 ? widep_tile_rows(P.p) : smallp_tile_rows(P); }

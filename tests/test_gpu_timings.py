@@ -20,7 +20,7 @@ def rows(engine, n, p, kind=0, n_int=2, seed=11):
 
 
 @pytest.mark.parametrize("n,p,chunk,launches", [(200_000, 9, 1 << 20, 2),   # small plan, one range: K1 K3a
-                                                (3_000_000, 16, 1 << 20, 3),  # small plan: K1 K3a K3b
+                                                (1_500_000, 16, 1 << 20, 3),  # small plan: K1 K3a K3b
                                                 (6_000_000, 16, 1 << 20, 4)])  # full tiles: gather K1 K3a K3b
 def test_timings_only_when_asked(engine, n, p, chunk, launches):
     from paper_2604_23826_b200 import DatasetSchema, ReductionPlan, ReductionTimings, plan_partitions
