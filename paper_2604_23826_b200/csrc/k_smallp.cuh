@@ -199,11 +199,38 @@ __device__ __forceinline__ void smallp_body(const TileJob& job) {
                 else step<NB>(x[u], c, acc, s);
             }
         }
-        for (; ks < nks; ks += kWarps, rowp += kstride) {
-            double x[NB];
-            load_row<NB, VEC>(rowp, g, p, x);
-            if (X1) step_x1<NB>(x, ld_stream(rowp + 8 * NB), c, ce, acc, s, ae, aee, se);
-            else step<NB>(x, c, acc, s);
+        if constexpr (TRC == 0 && NB <= 2) {
+            // runtime-height tiles (small plans, mostly one per CTA), p <= 17: the warp's last
+            // (< U) k-steps in predicated batches of 4 — a round trip per 4 k-steps instead of one
+            // each; k-steps past the tile read the shift row and add 0, like the ragged tail below
+            // (wider blocks keep the serial loop)
+            constexpr int UR = 4;
+            for (; ks < nks; ks += kWarps * UR, rowp += UR * kstride) {
+                double x[UR][NB], xe[UR];
+#pragma unroll
+                for (int u = 0; u < UR; ++u) {
+                    if (ks + kWarps * u < nks) {
+                        load_row<NB, VEC>(rowp + u * kstride, g, p, x[u]);
+                        if (X1) xe[u] = ld_stream(rowp + u * kstride + 8 * NB);
+                    } else {
+#pragma unroll
+                        for (int J = 0; J < NB; ++J) x[u][J] = c[J];
+                        xe[u] = ce;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UR; ++u) {
+                    if (X1) step_x1<NB>(x[u], xe[u], c, ce, acc, s, ae, aee, se);
+                    else step<NB>(x[u], c, acc, s);
+                }
+            }
+        } else {
+            for (; ks < nks; ks += kWarps, rowp += kstride) {
+                double x[NB];
+                load_row<NB, VEC>(rowp, g, p, x);
+                if (X1) step_x1<NB>(x, ld_stream(rowp + 8 * NB), c, ce, acc, s, ae, aee, se);
+                else step<NB>(x, c, acc, s);
+            }
         }
         // Ragged tail (rows % 4): the warp whose turn k-step nks is; missing rows add 0.
         if ((rows & 3) && warp == (int)(nks % kWarps)) {
