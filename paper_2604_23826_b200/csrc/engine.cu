@@ -444,12 +444,14 @@ struct Plan {
 
 // K1's tile height for a plan: kBigTileRows when the whole plan (every rank's ranges) has at
 // least kBigTileMin such tiles (C2: 6104) and p > 8 (p <= 8 measured 3 % slower with them);
-// kTileRows when it has at least kFillTiles of those; else — a plan too small to fill the GPU
-// with 4096-row tiles (C1: 245 tiles for 592 CTA slots) — the shortest height (a multiple of 32,
-// at least kMinTileRows) whose tiles fit one wave of K1's CTA slots (C1: 1696 rows, 590 tiles).
-// One wave measured best with L2 flushed before every call (C1 57.5 -> 48.8 us per call, 2e6 x 16
-// 82 -> 73 us; the previous rule, powers of two down to at least two waves, gave C1 512-row
-// tiles).  A function of the global plan alone: every rank and GPU count cuts the same tiles.
+// kTileRows when it has at least kFillTiles of those; else — a plan too small to fill two waves
+// of K1's CTA slots with 4096-row tiles (C1: 245 tiles for 592 slots) — the shortest height (a
+// multiple of 32, at least kMinTileRows) whose tiles fit as many whole waves as 4096-row tiles
+// would start: one (C1: 1696 rows, 590 tiles) or two (2.5e6 x 16: 2144 rows, 1168 tiles).
+// Measured with L2 flushed before every call (profiles/r02_small_plans_cold.log): C1 57.5 -> 48.8
+// us per call, 2e6 x 16 82 -> 73, 2.5e6 x 16 106 -> 85; the previous rule, powers of two down to
+// at least two waves, gave C1 512-row tiles.  A function of the global plan alone: every rank and
+// GPU count cuts the same tiles.
 uint64_t smallp_tile_rows(const Plan& P) {
     if (const char* env = getenv("SSTAT_K1_TILE_ROWS")) {  // experiment knob: a fixed height (multiple of 32)
         const uint64_t tr = strtoull(env, nullptr, 10);
@@ -457,19 +459,21 @@ uint64_t smallp_tile_rows(const Plan& P) {
     }
     if (P.p > 8 && P.total / kBigTileRows >= kBigTileMin) return kBigTileRows;
     if (P.total / kTileRows >= kFillTiles) return kTileRows;  // sum of ceil(count / TR) >= total / TR
-    if (P.R > kWaveTiles) return kTileRows;  // a tile per range at least: one wave is out of reach
     auto tiles_of = [&](uint64_t tr) {
         uint64_t t = 0;
         for (uint64_t i = 0; i < P.R; ++i) t += (P.counts[i] + tr - 1) / tr;
         return t;
     };
+    // as many whole waves as 4096-row tiles would start (one or two), each as short as they fit
+    const uint64_t target = tiles_of(kTileRows) > kWaveTiles ? kFillTiles : kWaveTiles;
+    if (P.R > target) return kTileRows;  // a tile per range at least
     // tiles_of falls as the height grows: the smallest multiple of 32 in [lo, kTileRows] that fits
-    uint64_t lo = std::max<uint64_t>(kMinTileRows, ((P.total + kWaveTiles - 1) / kWaveTiles + 31) / 32 * 32);
-    if (lo >= kTileRows || tiles_of(kTileRows) > kWaveTiles) return kTileRows;
-    uint64_t hi = kTileRows;  // fits
+    uint64_t lo = std::max<uint64_t>(kMinTileRows, ((P.total + target - 1) / target + 31) / 32 * 32);
+    if (lo >= kTileRows) return kTileRows;
+    uint64_t hi = kTileRows;  // fits: tiles_of(kTileRows) < kFillTiles here
     while (lo < hi) {
         const uint64_t mid = (lo + hi) / 2 / 32 * 32;
-        if (tiles_of(mid) <= kWaveTiles) hi = mid;
+        if (tiles_of(mid) <= target) hi = mid;
         else lo = mid + 32;
     }
     return hi;

@@ -12,6 +12,8 @@ from paper_2604_23826_b200 import DatasetSchema, Engine, ReductionPlan, plan_par
 CASES = [(1_000_000, 9, 1, 1 << 20), (1_000_000, 16, 0, 1 << 20), (2_000_000, 16, 0, 1 << 20),
          (4_000_000, 16, 0, 1 << 20), (2_000_000, 8, 0, 1 << 20), (300_000, 32, 0, 1 << 20),
          (3_000_000, 9, 1, 100_000), (500_000, 24, 0, 1 << 20)]
+if os.environ.get("COLD_CASES"):  # n:p:kind:chunk,...
+    CASES = [tuple(int(float(v)) for v in c.split(":")) for c in os.environ["COLD_CASES"].split(",")]
 eng = Engine(0)
 s = torch.cuda.current_stream()
 eng.set_stream(s.cuda_stream)
