@@ -442,6 +442,8 @@ def run_ours(args):
                    "k1_frac": n1 * p1 * 8 / (k1_us * 1e-6) / 1e9 / hbm_peak,
                    "kernel": eng.last_timings.kernel.decode(), "calls": len(calls),
                    "l2": "flushed before every call (a 256 MB read)",
+                   "k1_note": "k1_us by the two graph event nodes around K1 (a few us of node time at this size; "
+                              "ncu's cold capture: 20.7 us, profiles/r02_k1_c1_full.md)",
                    "what": "dataset_suffstats(CUDA tensor) of 1e6 rows x (8 + ID): K1 on one wave of tiles, K3a, "
                            "read-back, one replayed graph; call_us = device time from before the call to after "
                            "its return (medians over 200 calls)"}
