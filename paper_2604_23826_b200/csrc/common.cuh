@@ -18,7 +18,8 @@ constexpr uint32_t kTileRows = 4096;
 constexpr uint32_t kBigTileRows = 16384;
 constexpr uint32_t kMinTileRows = 256;
 constexpr uint64_t kFillTiles = 2ull * 148 * 4;   // twice K1's resident CTA slots on a B200
-constexpr uint64_t kWaveTiles = 148ull * 4;       // K1's resident CTA slots on a B200
+constexpr uint64_t kWaveTiles = 148ull * 4;       // K1's resident CTA slots on a B200 (4 per SM)
+constexpr uint64_t kWaveSMs = 148;                // the SMs a tile wave is counted over (B200)
 constexpr uint64_t kBigTileMin = 8ull * 148 * 4;  // eight waves of big tiles
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
@@ -53,6 +54,8 @@ struct TileJob {
     uint32_t tile_rows;            // K1: rows per tile of this plan (smallp_tile_rows)
     uint32_t shift_in_place;       // K1 runtime-height instances, shift == nullptr: the shift row is
                                    // the range's first row read from base (a resident shard)
+    int* occupancy;                // K1 query (non-null): receives the CTAs per SM of the kernel the
+                                   // launcher would choose; nothing is launched
 };
 
 // Range owning tile t (tile_prefix ascending; binary search, O(log R) L2 reads per tile).

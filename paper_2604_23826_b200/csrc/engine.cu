@@ -464,13 +464,17 @@ uint64_t smallp_tile_rows(const Plan& P) {
         for (uint64_t i = 0; i < P.R; ++i) t += (P.counts[i] + tr - 1) / tr;
         return t;
     };
-    // as many whole waves as 4096-row tiles would start (one or two), each as short as they fit
-    const uint64_t target = tiles_of(kTileRows) > kWaveTiles ? kFillTiles : kWaveTiles;
+    // as many whole waves as 4096-row tiles would start (one or two), each as short as they fit; a
+    // wave is kWaveSMs x the CTAs per SM of the kernel this width runs (4 up to p = 16, 3 at
+    // p = 24-32, 2 at p = 40-64: C1 592 slots, p = 32 444)
+    const uint64_t wave = kWaveSMs * smallp_rt_ctas_per_sm(P.p);
+    if (tiles_of(kTileRows) > 2 * wave) return kTileRows;
+    const uint64_t target = tiles_of(kTileRows) > wave ? 2 * wave : wave;
     if (P.R > target) return kTileRows;  // a tile per range at least
     // tiles_of falls as the height grows: the smallest multiple of 32 in [lo, kTileRows] that fits
     uint64_t lo = std::max<uint64_t>(kMinTileRows, ((P.total + target - 1) / target + 31) / 32 * 32);
     if (lo >= kTileRows) return kTileRows;
-    uint64_t hi = kTileRows;  // fits: tiles_of(kTileRows) < kFillTiles here
+    uint64_t hi = kTileRows;  // fits: tiles_of(kTileRows) <= target here
     while (lo < hi) {
         const uint64_t mid = (lo + hi) / 2 / 32 * 32;
         if (tiles_of(mid) <= target) hi = mid;

@@ -332,6 +332,10 @@ cudaError_t launch_nb_x1(const TileJob& job, int sms, cudaStream_t stream) {
         if (per_sm < 1) per_sm = 1;
         if (dev < 64) cached[dev].store(per_sm);
     }
+    if (job.occupancy) {
+        *job.occupancy = per_sm;
+        return cudaSuccess;
+    }
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;
     if (grid == 0) return cudaSuccess;
@@ -369,6 +373,10 @@ cudaError_t launch_nb(const TileJob& job, int sms, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
         if (dev < 64) cached[variant][dev].store(per_sm);
+    }
+    if (job.occupancy) {
+        *job.occupancy = per_sm;
+        return cudaSuccess;
     }
     const uint64_t tiles = job.tile_end - job.tile_begin;
     const uint64_t grid = tiles < (uint64_t)sms * per_sm ? tiles : (uint64_t)sms * per_sm;

@@ -11,6 +11,10 @@ namespace sstat_b200 {
 // K1: tiles [job.tile_begin, job.tile_end), p <= 64; persistent grid of
 // min(tiles, sms x resident CTAs per SM).
 cudaError_t launch_smallp(const TileJob& job, int sms, cudaStream_t stream);
+// CTAs per SM of the runtime-height K1 kernel for width p (alignment-independent): the wave size
+// of the small-plan tile rule (smallp_tile_rows).
+constexpr uint32_t kMaxSmallP = 64;
+uint32_t smallp_rt_ctas_per_sm(uint32_t p);
 
 // K1w: 64 < p <= 128 (splitp_handles), K1's register-direct pass with the triangle split over
 // warps; tiles of widep_tile_rows(p) rows like K2.
